@@ -1,0 +1,131 @@
+/* kvmix_b200.h -- C ABI of the B200-native TriAxialKV hot path (libkvmix_b200.so).
+ *
+ * Plain pointers and sizes only: no torch, no C++ types.  Every device pointer is
+ * a CUDA device address; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Every entry point is asynchronous on `stream` unless stated otherwise and returns
+ * a status code; kvmix_last_error() gives the message of the last failure on the
+ * calling thread.  Each entry point cites the reference (kvmix, /root/reference/pkg)
+ * interface it replaces -- see INTEGRATION.md for the ctypes binding.
+ *
+ * Device pool layout, G = 32, d = head_dim:
+ *   int2_pool : uint8 [L][Hkv][n_pages][page_stride(d)]
+ *               record = KeyPageBlock (d*G/4 + 4d B) || G INT2 V TokenBlocks (d/4 + 4d/G B each)
+ *   int4_pool : uint8 [L][Hkv][n_int4][slot_stride(d)]
+ *               record = INT4 K TokenBlock (d/2 + 4d/G B) || INT4 V TokenBlock
+ * Each block is the reference payload byte-for-byte (LAYOUT.md); strides round up to 16 B.
+ * Slot s < offset is INT2 page s/G row s%G; slot s >= offset is INT4 index s - offset.
+ */
+#ifndef KVMIX_B200_H
+#define KVMIX_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVMIX_GROUP_SIZE 32 /* quant.py:23 GROUP_SIZE */
+
+/* status codes */
+#define KVMIX_OK 0
+#define KVMIX_EINVAL (-2)    /* reference ValidationError (errors.py:12) */
+#define KVMIX_ECAPACITY (-3) /* reference CapacityError (errors.py:27) */
+#define KVMIX_ECUDA (-5)     /* CUDA launch/runtime failure */
+
+/* element types of float inputs/outputs */
+#define KVMIX_F32 0
+#define KVMIX_BF16 1
+#define KVMIX_F16 2
+
+const char* kvmix_version(void);
+const char* kvmix_last_error(void);
+/* record strides of the device pools (bytes) */
+int64_t kvmix_page_stride(int64_t head_dim);
+int64_t kvmix_slot_stride(int64_t head_dim);
+/* payload sizes; replace quant.py:123-128 key_page_payload_bytes / token_block_payload_bytes */
+int64_t kvmix_key_page_payload_bytes(int64_t head_dim);
+int64_t kvmix_token_block_payload_bytes(int64_t head_dim, int64_t bitwidth);
+
+/* ---- codec (K1) --------------------------------------------------------------- */
+
+/* Replaces quant.py:160 encode_key_page_int2 (batched): keys f32 [n_pages][G][d] ->
+ * out [n_pages][out_stride] with the KeyPageBlock payload at the start of each row.
+ * err_flag (device int32, may be NULL) gets bit 0 set on non-finite input. */
+int kvmix_encode_key_pages(const float* keys, int64_t n_pages, int64_t head_dim, uint8_t* out, int64_t out_stride,
+                           int32_t* err_flag, void* stream);
+/* Replaces quant.py:189 encode_token_block / :206 encode_token_blocks:
+ * x f32 [n][d] -> out [n][out_stride], TokenBlock payload at the start of each row. */
+int kvmix_encode_token_blocks(const float* x, int64_t n, int64_t head_dim, int32_t bitwidth, uint8_t* out,
+                              int64_t out_stride, int32_t* err_flag, void* stream);
+/* Replaces quant.py:180 decode_key_page_int2: blocks [n_pages][in_stride] -> f32 [n_pages][G][d] */
+int kvmix_decode_key_pages(const uint8_t* blocks, int64_t n_pages, int64_t head_dim, int64_t in_stride, float* out,
+                           void* stream);
+/* Replaces quant.py:235 decode_token_blocks / :256 decode_token_block: [n][in_stride] -> f32 [n][d] */
+int kvmix_decode_token_blocks(const uint8_t* blocks, int64_t n, int64_t head_dim, int32_t bitwidth,
+                              int64_t in_stride, float* out, void* stream);
+/* Replaces quant.py:64 quantize_group (batched, ragged): groups are x[offsets[i]:offsets[i+1]],
+ * codes written at the same positions, scale/zero per group (fp32 holding the fp16 value). */
+int kvmix_quantize_groups(const float* x, const int64_t* offsets, int64_t n_groups, int32_t bitwidth,
+                          uint8_t* codes, float* scale, float* zero, int32_t* err_flag, void* stream);
+/* Replaces quant.py:96 pack_codes / :112 unpack_codes. n codes <-> ceil(n*b/8) bytes.
+ * pack sets err_flag bit 1 if a code is out of range. */
+int kvmix_pack_codes(const uint8_t* codes, int64_t n, int32_t bitwidth, uint8_t* out, int32_t* err_flag,
+                     void* stream);
+int kvmix_unpack_codes(const uint8_t* packed, int64_t n, int32_t bitwidth, uint8_t* out, void* stream);
+
+/* ---- pool data plane ------------------------------------------------------------- */
+
+/* Replaces pool.py:228 MixedPrecisionPool.write_prefill (with write_page :201 and the INT4
+ * branch :253-262): quantize+pack one request's prefill K/V [L][n_tokens][Hkv][d]
+ * (dtype KVMIX_F32/BF16/F16, contiguous) into the pools.
+ * page_tokens [n_req_pages][G]: token index of each page row (token order);
+ * page_ids [n_req_pages]: destination page index; int4_tokens/int4_ids [n_req_int4]. */
+int kvmix_write_prefill(const void* keys, const void* values, int32_t dtype, int64_t n_layers, int64_t n_tokens,
+                        int64_t n_kv_heads, int64_t head_dim, const int32_t* page_tokens, const int32_t* page_ids,
+                        int64_t n_req_pages, const int32_t* int4_tokens, const int32_t* int4_ids,
+                        int64_t n_req_int4, uint8_t* int2_pool, int64_t pool_pages, uint8_t* int4_pool,
+                        int64_t pool_int4, int32_t* err_flag, void* stream);
+
+/* Replaces pool.py:284 append_decode_token (data half; the host pops the slot) and
+ * pool.py:217 write_token: quantize n tokens' K/V [n][n_layers_in][Hkv][d] at INT4 into
+ * int4 indices int4_ids[n], pool layers [layer0, layer0 + n_layers_in). */
+int kvmix_append_int4(const void* k, const void* v, int32_t dtype, int64_t n, int64_t n_layers_in, int64_t layer0,
+                      int64_t n_layers, int64_t n_kv_heads, int64_t head_dim, const int32_t* int4_ids,
+                      uint8_t* int4_pool, int64_t pool_int4, int32_t* err_flag, void* stream);
+
+/* Replaces pool.py:394 PoolView.gather and pool.py:264 read_slot (K5): decode slots[m]
+ * of one layer into k_out, v_out f32 [m][Hkv][d]. */
+int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4,
+                         int64_t offset, int64_t layer, int64_t n_kv_heads, int64_t head_dim, const int32_t* slots,
+                         int64_t m, float* k_out, float* v_out, void* stream);
+
+/* ---- decode attention (K2 + K3) ---------------------------------------------------- */
+
+/* Replaces attention.py:175 flash_decode (+ PoolView.gather pool.py:394, _split_partial
+ * attention.py:168, merge_partials attention.py:154), batched over requests, one layer.
+ *   q [batch][n_q_heads][d] (q_dtype), out [batch][n_q_heads][d] (out_dtype)
+ *   page_indptr[batch+1], page_ids[]: INT2 page list of each partitioned table (table order)
+ *   int4_indptr[batch+1], int4_ids[]: INT4 indices of each table's suffix (table order)
+ *   work [n_work][4] = {unit = b*Hkv + kvh, tile_lo, tile_hi, partial_slot}; the tiles of a
+ *     unit are its INT2 pages then ceil(n_int4/32) INT4 tiles of 32 slots (splits are
+ *     bitwidth-homogeneous per tile, never straddling pages)
+ *   part_indptr[batch*Hkv + 1]: partial slots of each unit (contiguous)
+ *   workspace: >= n_parts * (n_q_heads/Hkv) * (d + 2) floats
+ *   variant: 0 = tensor-core kernel (mma.sync m16n8k16), 1 = simple CUDA-core kernel
+ * Requires n_q_heads % Hkv == 0 and n_q_heads / Hkv <= 8, d in {32, 64, 128}. */
+int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype, const uint8_t* int2_pool,
+                       const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
+                       int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
+                       const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
+                       const int32_t* int4_ids, const int32_t* work, int64_t n_work, const int32_t* part_indptr,
+                       float* workspace, int64_t workspace_floats, float scale, int32_t variant, void* stream);
+
+/* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
+ * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */
+int kvmix_merge_partials(const float* acc, const float* lse, const float* max_logit, int64_t n, int64_t d, float* out,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVMIX_B200_H */

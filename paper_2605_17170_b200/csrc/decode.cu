@@ -1,0 +1,647 @@
+// K2 split-K mixed INT2/INT4 decode attention + K3 cross-split combine.
+//
+// Replaces attention.py:175-218 flash_decode (+ PoolView.gather pool.py:394-439,
+// _split_partial attention.py:168-172, merge_partials attention.py:154-165), batched
+// over requests for one layer.  Work item = (request, kv head, contiguous tile range);
+// a tile is one INT2 page (32 tokens) or 32 INT4 slots, so every tile is
+// bitwidth-homogeneous like the reference's splits.  Softmax runs in the log2 domain
+// (q is pre-scaled by scale*log2(e)); partials are (acc[d], m, l) per q head.
+//
+// Tensor-core kernel (variant 0), one warp = one independent flash-decoding stream:
+//  * each warp owns a STAGES-deep smem ring filled by cp.async.bulk (TMA bulk copies,
+//    one 3 KB copy per INT2 page, one per INT4 slot) completing on mbarriers;
+//  * QK^T as S^T[token x head] = K[token x ch] . Q^T with mma.sync m16n8k16 (N = 8 =
+//    the GQA group): INT2 key pages fold the per-channel scale into q (q' = q*s per
+//    page) and add the per-page bias sum_c q_c z_c with one extra MMA whose A rows are
+//    the zeros; INT4 keys are dequantised in registers;
+//  * P goes C-fragment -> B-fragment with movmatrix;
+//  * PV as O^T[ch x head] = V^T . P'^T with group-pure M tiles so the per-token
+//    group scale folds into P' = p*s, and sum_t p*z comes from an MMA with A = 1;
+//  * codes become fp16 with one LOP3 against the 0x3C00 exponent (1 + code*2^(p-10))
+//    and an exact HSUB2, leaving code * 2^(p-10); the power of two is undone per row.
+#include "common.cuh"
+#include "launch.h"
+
+namespace kvmix {
+
+constexpr int NW = 4;      // warps per CTA
+constexpr int STAGES = 4;  // ring depth per warp
+constexpr uint32_t MAGIC = 0x3C003C00u;
+constexpr float LOG2E = 1.4426950408889634f;
+
+template <int D>
+struct Cfg {
+  static constexpr int NCH = D / 16;   // QK k-chunks == PV M tiles
+  static constexpr int NGRP = D / 32;  // channel groups
+  static constexpr int KP = key_page_bytes(D);
+  static constexpr int TB2 = tok_bytes(D, 2);
+  static constexpr int TB4 = tok_bytes(D, 4);
+  static constexpr int PS = page_stride(D);
+  static constexpr int SS = slot_stride(D);
+  static constexpr int SSM = D == 128 ? 176 : (D == 64 ? 80 : 48);  // smem slot stride, == 16 mod 32 (bank spread)
+  static constexpr int BUF = PS > 32 * SSM ? PS : 32 * SSM;
+  static constexpr int SMEM = NW * STAGES * BUF;
+};
+
+struct DecodeArgs {
+  const void* q;
+  int q_dtype;
+  void* out;
+  int out_dtype;
+  const uint8_t* int2_pool;
+  const uint8_t* int4_pool;
+  int64_t pool_pages, pool_int4, layer;
+  int n_kv, n_q, gq, batch;
+  const int32_t* page_indptr;
+  const int32_t* page_ids;
+  const int32_t* int4_indptr;
+  const int32_t* int4_ids;
+  const int32_t* work;
+  const int32_t* part_indptr;
+  float* ws;
+  float qscale;  // softmax scale * log2(e)
+};
+
+__device__ __forceinline__ float load_q(const DecodeArgs& a, int64_t idx) {
+  if (a.q_dtype == KVMIX_F32) return reinterpret_cast<const float*>(a.q)[idx];
+  if (a.q_dtype == KVMIX_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[idx]);
+  return __half2float(reinterpret_cast<const __half*>(a.q)[idx]);
+}
+
+template <int NG>
+__device__ __forceinline__ void lds_params(const uint8_t* p, uint32_t (&w)[NG]) {
+  if constexpr (NG == 4) {
+    uint4 v = *reinterpret_cast<const uint4*>(p);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  } else if constexpr (NG == 2) {
+    uint2 v = *reinterpret_cast<const uint2*>(p);
+    w[0] = v.x; w[1] = v.y;
+  } else {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  }
+}
+__device__ __forceinline__ uint32_t lds32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+// code * 2^(2e-10) for the 2-bit field e of each half (INT2 codes in bits 2e..2e+1)
+__device__ __forceinline__ uint32_t int2_field(uint32_t r, int e) {
+  return hsub2u(lop_and_or(r, 0x00030003u << (2 * e), MAGIC), MAGIC);
+}
+
+// ------------------------------------------------------------------------------------
+// Work-item prologue shared by both kernel variants.
+struct Unit {
+  int b, kvh, tlo, thi, part, npg, n4;
+  int64_t pg0, i40;
+};
+__device__ __forceinline__ Unit load_unit(const DecodeArgs& a) {
+  const int32_t* wk = a.work + 4 * (int64_t)blockIdx.x;
+  Unit u;
+  const int unit = wk[0];
+  u.b = unit / a.n_kv;
+  u.kvh = unit % a.n_kv;
+  u.tlo = wk[1];
+  u.thi = wk[2];
+  u.part = wk[3];
+  u.pg0 = a.page_indptr[u.b];
+  u.npg = a.page_indptr[u.b + 1] - (int)u.pg0;
+  u.i40 = a.int4_indptr[u.b];
+  u.n4 = a.int4_indptr[u.b + 1] - (int)u.i40;
+  return u;
+}
+
+// Merge the NW warps' (m, l, acc) per head through smem and write the work item's partial.
+template <int D>
+__device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit& u, float* sm_m, float* sm_l,
+                                                float* sm_acc) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
+    const int hh = i / D, c = i % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_m[w * 8 + hh]);
+    float acc = 0.f, l = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float mw = sm_m[w * 8 + hh];
+      const float f = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
+      acc += f * sm_acc[(w * 8 + hh) * D + c];
+      l += f * sm_l[w * 8 + hh];
+    }
+    float* dst = a.ws + ((int64_t)u.part * a.gq + hh) * (D + 2);
+    dst[c] = acc;
+    if (c == 0) {
+      dst[D] = M;
+      dst[D + 1] = l;
+    }
+  }
+}
+
+// ====================================================================================
+// Variant 0: tensor-core kernel.
+template <int D>
+__global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs a) {
+  using C = Cfg<D>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[NW][STAGES];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const Unit u = load_unit(a);
+  uint8_t* ring = smem + warp * STAGES * C::BUF;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[warp][s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // ---- Q fragments (B operand of QK), fp16, pre-scaled by scale*log2(e) ----
+  // qb2: INT2 key pages, chunk i covers channels 16i..16i+15 in natural order.
+  // qb4: INT4 keys, chunk 2j+s pairs channels (32j+8q+{0,4}/{1,5}) (s=0) or ({2,6}/{3,7}) (s=1).
+  uint32_t qb2[C::NCH][2], qb4[C::NCH][2];
+  {
+    const bool hv = g < a.gq;
+    const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
+    auto qv = [&](int c) { return hv ? load_q(a, qrow + c) * a.qscale : 0.f; };
+#pragma unroll
+    for (int i = 0; i < C::NCH; ++i) {
+      const int c1 = 16 * i + 2 * q;
+      qb2[i][0] = pack_h2(qv(c1), qv(c1 + 1));
+      qb2[i][1] = pack_h2(qv(c1 + 8), qv(c1 + 9));
+      const int base = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
+      qb4[i][0] = pack_h2(qv(base + 0), qv(base + 4));
+      qb4[i][1] = pack_h2(qv(base + 1), qv(base + 5));
+    }
+  }
+
+  // ---- tile enumeration for this warp ----
+  const int ntiles = u.thi - u.tlo;
+  const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
+  const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
+  const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
+
+  auto issue = [&](int k) {
+    const int t = u.tlo + warp + k * NW;
+    const int s = k % STAGES;
+    uint8_t* buf = ring + s * C::BUF;
+    uint64_t* bar = &bars[warp][s];
+    if (t < u.npg) {
+      if (lane == 0) {
+        const int64_t page = a.page_ids[u.pg0 + t];
+        mbar_expect_tx(bar, C::PS);
+        bulk_g2s(buf, kv2 + page * C::PS, C::PS, bar);
+      }
+    } else {
+      const int it = t - u.npg;
+      const int nv = min(32, u.n4 - 32 * it);
+      if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
+      __syncwarp();
+      if (lane < nv) {
+        const int64_t slot = a.int4_ids[u.i40 + 32 * it + lane];
+        bulk_g2s(buf + lane * C::SSM, kv4 + slot * C::SS, C::SS, bar);
+      }
+    }
+  };
+
+  for (int k = 0; k < STAGES && k < nmine; ++k) issue(k);
+
+  // ---- running state ----
+  float o[C::NCH][4];    // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
+  float zs[C::NGRP][4];  // sum_t p * z per channel group
+#pragma unroll
+  for (int m = 0; m < C::NCH; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < C::NGRP; ++j) zs[j][0] = zs[j][1] = zs[j][2] = zs[j][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  // INT2 page row map: lane g reads byte beta(g) of every channel word (tokens 4beta..4beta+3).
+  const uint32_t selK = (uint32_t)(g >> 1) | ((uint32_t)(4 + (g >> 1)) << 8);
+  const int koff = 4 * (g & 1);
+  const uint32_t selV2 = (uint32_t)(g & 3) | ((uint32_t)(4 + (g & 3)) << 8);
+  const int voff2 = 4 * (g >> 2);
+  const uint32_t b4 = 2 * (g & 1);
+  const uint32_t selV4 = b4 | ((b4 + 1) << 4) | ((b4 + 4) << 8) | ((b4 + 5) << 12);
+  const int voff4 = 4 * (g >> 1);
+
+  for (int k = 0; k < nmine; ++k) {
+    const int t = u.tlo + warp + k * NW;
+    const int s = k % STAGES;
+    const uint8_t* buf = ring + s * C::BUF;
+    mbar_wait(&bars[warp][s], (uint32_t)((k / STAGES) & 1));
+
+    float sv[8];  // S (log2 domain) for rows {M0: g, g+8; M1: g, g+8} x heads {2q, 2q+1}
+    const bool is2 = t < u.npg;
+    int nv = 32;
+    // PV token pairs (smem offsets of the 4 token records of each k-step) and params
+    if (is2) {
+      // ---------------- QK over an INT2 key page ----------------
+      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1v[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint8_t* kc = buf + koff;
+      const uint8_t* kpar = buf + 8 * D;
+#pragma unroll
+      for (int i = 0; i < C::NCH; ++i) {
+        const int ca = 16 * i + 2 * q, cc = ca + 8;
+        const uint32_t r1 = prmt(lds32(kc + 8 * ca), lds32(kc + 8 * ca + 8), selK);
+        const uint32_t r2 = prmt(lds32(kc + 8 * cc), lds32(kc + 8 * cc + 8), selK);
+        const uint2 p1 = *reinterpret_cast<const uint2*>(kpar + 4 * ca);
+        const uint2 p2 = *reinterpret_cast<const uint2*>(kpar + 4 * cc);
+        const uint32_t z1 = prmt(p1.x, p1.y, 0x7632), z2 = prmt(p2.x, p2.y, 0x7632);
+        const uint32_t qa = hmul2u(qb2[i][0], prmt(p1.x, p1.y, 0x5410));
+        const uint32_t qc = hmul2u(qb2[i][1], prmt(p2.x, p2.y, 0x5410));
+        mma16816(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qa, qc);
+        mma16816(c1v, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qa, qc);
+        mma16816(cb, z1, z1, z2, z2, qb2[i][0], qb2[i][1]);
+      }
+      // undo 2^(2k-10) per token row (k = position of the token inside its code byte)
+      sv[0] = fmaf(c0[0], 1024.f, cb[0]);
+      sv[1] = fmaf(c0[1], 1024.f, cb[1]);
+      sv[2] = fmaf(c0[2], 256.f, cb[0]);
+      sv[3] = fmaf(c0[3], 256.f, cb[1]);
+      sv[4] = fmaf(c1v[0], 64.f, cb[0]);
+      sv[5] = fmaf(c1v[1], 64.f, cb[1]);
+      sv[6] = fmaf(c1v[2], 16.f, cb[0]);
+      sv[7] = fmaf(c1v[3], 16.f, cb[1]);
+    } else {
+      // ---------------- QK over INT4 keys (dequantised in registers) ----------------
+      nv = min(32, u.n4 - 32 * (t - u.npg));
+      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < C::NGRP; ++j) {
+        uint32_t e[4][4];  // [slot row: M0 g, M0 g+8, M1 g, M1 g+8][field]
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint8_t* rec = buf + C::SSM * (16 * (r >> 1) + g + 8 * (r & 1));
+          const uint32_t w = lds32(rec + 16 * j + 4 * q);
+          const uint32_t par = lds32(rec + D / 2 + 4 * j);
+          const uint32_t s16 = hmul2u(prmt(par, par, 0x1010), 0x4C004C00u);  // (16s, 16s)
+          const uint32_t zz = prmt(par, par, 0x3232);
+          e[r][0] = hfma2u(hsub2u(lop_and_or(w << 6, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
+          e[r][1] = hfma2u(hsub2u(lop_and_or(w << 2, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
+          e[r][2] = hfma2u(hsub2u(lop_and_or(w >> 2, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
+          e[r][3] = hfma2u(hsub2u(lop_and_or(w >> 6, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
+        }
+        mma16816(c0, e[0][0], e[1][0], e[0][1], e[1][1], qb4[2 * j][0], qb4[2 * j][1]);
+        mma16816(c0, e[0][2], e[1][2], e[0][3], e[1][3], qb4[2 * j + 1][0], qb4[2 * j + 1][1]);
+        mma16816(c1v, e[2][0], e[3][0], e[2][1], e[3][1], qb4[2 * j][0], qb4[2 * j][1]);
+        mma16816(c1v, e[2][2], e[3][2], e[2][3], e[3][3], qb4[2 * j + 1][0], qb4[2 * j + 1][1]);
+      }
+      sv[0] = (g < nv) ? c0[0] : -INFINITY;
+      sv[1] = (g < nv) ? c0[1] : -INFINITY;
+      sv[2] = (g + 8 < nv) ? c0[2] : -INFINITY;
+      sv[3] = (g + 8 < nv) ? c0[3] : -INFINITY;
+      sv[4] = (g + 16 < nv) ? c1v[0] : -INFINITY;
+      sv[5] = (g + 16 < nv) ? c1v[1] : -INFINITY;
+      sv[6] = (g + 24 < nv) ? c1v[2] : -INFINITY;
+      sv[7] = (g + 24 < nv) ? c1v[3] : -INFINITY;
+    }
+
+    // ---------------- online softmax (log2 domain) ----------------
+    float tm0 = fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6]));
+    float tm1 = fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7]));
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
+      tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
+    }
+    const float mn0 = fmaxf(m0, tm0), mn1 = fmaxf(m1, tm1);
+    const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);  // exp2(-inf) = 0
+    m0 = mn0;
+    m1 = mn1;
+    float p[8];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      p[i] = fast_exp2(sv[i] - mn0);
+      p[i + 1] = fast_exp2(sv[i + 1] - mn1);
+    }
+    l0 = l0 * al0 + (p[0] + p[2]) + (p[4] + p[6]);
+    l1 = l1 * al1 + (p[1] + p[3]) + (p[5] + p[7]);
+    if (__any_sync(0xffffffffu, (al0 != 1.f) || (al1 != 1.f))) {
+#pragma unroll
+      for (int m = 0; m < C::NCH; ++m) {
+        o[m][0] *= al0; o[m][2] *= al0;
+        o[m][1] *= al1; o[m][3] *= al1;
+      }
+#pragma unroll
+      for (int j = 0; j < C::NGRP; ++j) {
+        zs[j][0] *= al0; zs[j][2] *= al0;
+        zs[j][1] *= al1; zs[j][3] *= al1;
+      }
+    }
+    // P^T B fragments for PV k-steps 0, 1 (k index == QK row): lane holds head g,
+    // rows (2q, 2q+1) in bP[ks][0] and (2q+8, 2q+9) in bP[ks][1].
+    uint32_t bP[2][2];
+    bP[0][0] = movtrans(pack_h2(p[0], p[1]));
+    bP[0][1] = movtrans(pack_h2(p[2], p[3]));
+    bP[1][0] = movtrans(pack_h2(p[4], p[5]));
+    bP[1][1] = movtrans(pack_h2(p[6], p[7]));
+
+    // ---------------- PV ----------------
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      // smem records of the pair-A tokens (k = 2q, 2q+1) and pair-B tokens (2q+8, 2q+9)
+      const uint8_t *vA0, *vA1, *vB0, *vB1;
+      bool okA0 = true, okA1 = true, okB0 = true, okB1 = true;
+      if (is2) {
+        const int tA0 = 4 * q + 2 * ks, tA1 = 16 + 4 * q + 2 * ks;
+        const uint8_t* vb = buf + C::KP;
+        vA0 = vb + C::TB2 * tA0;
+        vA1 = vb + C::TB2 * tA1;
+        vB0 = vA0 + C::TB2;
+        vB1 = vA1 + C::TB2;
+      } else {
+        const int sA0 = 16 * ks + 2 * q;
+        vA0 = buf + C::SSM * sA0 + C::TB4;
+        vA1 = vA0 + C::SSM;
+        vB0 = vA0 + 8 * C::SSM;
+        vB1 = vB0 + C::SSM;
+        okA0 = sA0 < nv;
+        okA1 = sA0 + 1 < nv;
+        okB0 = sA0 + 8 < nv;
+        okB1 = sA0 + 9 < nv;
+      }
+      const int poff = is2 ? D / 4 : D / 2;
+      uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
+      lds_params<C::NGRP>(vA0 + poff, pA0);
+      lds_params<C::NGRP>(vA1 + poff, pA1);
+      lds_params<C::NGRP>(vB0 + poff, pB0);
+      lds_params<C::NGRP>(vB1 + poff, pB1);
+#pragma unroll
+      for (int j = 0; j < C::NGRP; ++j) {
+        if (!okA0) pA0[j] = 0u;
+        if (!okA1) pA1[j] = 0u;
+        if (!okB0) pB0[j] = 0u;
+        if (!okB1) pB1[j] = 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < C::NGRP; ++j) {
+        uint32_t rA, rB;
+        uint32_t fA[4], fB[4];
+        if (is2) {
+          rA = prmt(lds32(vA0 + 8 * j + voff2), lds32(vA1 + 8 * j + voff2), selV2);
+          rB = prmt(lds32(vB0 + 8 * j + voff2), lds32(vB1 + 8 * j + voff2), selV2);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            fA[e] = int2_field(rA, e);
+            fB[e] = int2_field(rB, e);
+          }
+        } else {
+          rA = prmt(lds32(vA0 + 16 * j + voff4), lds32(vA1 + 16 * j + voff4), selV4);
+          rB = prmt(lds32(vB0 + 16 * j + voff4), lds32(vB1 + 16 * j + voff4), selV4);
+          fA[0] = hsub2u(lop_and_or(rA, 0x000F000Fu, MAGIC), MAGIC);
+          fA[1] = hsub2u(lop_and_or(rA >> 2, 0x003C003Cu, MAGIC), MAGIC);
+          fA[2] = hsub2u(lop_and_or(rA >> 4, 0x00F000F0u, MAGIC), MAGIC);
+          fA[3] = hsub2u(lop_and_or(rA >> 6, 0x03C003C0u, MAGIC), MAGIC);
+          fB[0] = hsub2u(lop_and_or(rB, 0x000F000Fu, MAGIC), MAGIC);
+          fB[1] = hsub2u(lop_and_or(rB >> 2, 0x003C003Cu, MAGIC), MAGIC);
+          fB[2] = hsub2u(lop_and_or(rB >> 4, 0x00F000F0u, MAGIC), MAGIC);
+          fB[3] = hsub2u(lop_and_or(rB >> 6, 0x03C003C0u, MAGIC), MAGIC);
+        }
+        // P' = p * s (per token, group j) and P*z, as B fragments
+        const uint32_t sA = prmt(pA0[j], pA1[j], 0x5410), zA = prmt(pA0[j], pA1[j], 0x7632);
+        const uint32_t sB = prmt(pB0[j], pB1[j], 0x5410), zB = prmt(pB0[j], pB1[j], 0x7632);
+        const uint32_t ps0 = hmul2u(bP[ks][0], sA), ps1 = hmul2u(bP[ks][1], sB);
+        const uint32_t pz0 = hmul2u(bP[ks][0], zA), pz1 = hmul2u(bP[ks][1], zB);
+        mma16816(o[2 * j], fA[0], fA[1], fB[0], fB[1], ps0, ps1);
+        mma16816(o[2 * j + 1], fA[2], fA[3], fB[2], fB[3], ps0, ps1);
+        mma16816(zs[j], MAGIC, MAGIC, MAGIC, MAGIC, pz0, pz1);
+      }
+    }
+
+    __syncwarp();
+    if (k + STAGES < nmine) {
+      fence_proxy_async();
+      issue(k + STAGES);
+    }
+  }
+
+  // ---- finalize this warp: full l per head, acc[h][c] = 2^(10-2e) * O^T + zsum ----
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+  }
+  __syncthreads();  // all warps done with their rings -> reuse smem for the merge
+  float* sm_acc = reinterpret_cast<float*>(smem);
+  float* sm_m = sm_acc + NW * 8 * D;
+  float* sm_l = sm_m + NW * 8;
+#pragma unroll
+  for (int m = 0; m < C::NCH; ++m) {
+    const int j = m >> 1;
+    const int e0 = 2 * (m & 1);
+    const int ch0 = 32 * j + 4 * g + e0;
+    const float f0 = (float)(1 << (10 - 2 * e0)), f1 = (float)(1 << (10 - 2 * (e0 + 1)));
+    sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(o[m][0], f0, zs[j][0]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(o[m][1], f0, zs[j][1]);
+    sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(o[m][2], f1, zs[j][0]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(o[m][3], f1, zs[j][1]);
+  }
+  if (g == 0) {
+    sm_m[warp * 8 + 2 * q] = m0;
+    sm_m[warp * 8 + 2 * q + 1] = m1;
+    sm_l[warp * 8 + 2 * q] = l0;
+    sm_l[warp * 8 + 2 * q + 1] = l1;
+  }
+  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc);
+}
+
+// ====================================================================================
+// Variant 1: simple CUDA-core kernel (fp32 dequant straight from HBM).  Slow; kept as
+// an independent on-GPU cross-check of the tensor-core kernel at full sizes.
+template <int D>
+__global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs a) {
+  constexpr int CPL = D / 32;
+  __shared__ float qs[8][D];
+  __shared__ float sm_acc[NW * 8 * D];
+  __shared__ float sm_m[NW * 8], sm_l[NW * 8];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  const Unit u = load_unit(a);
+  for (int i = threadIdx.x; i < 8 * D; i += blockDim.x) {
+    const int hh = i / D, c = i % D;
+    qs[hh][c] = hh < a.gq ? load_q(a, ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + hh) * D + c) * a.qscale : 0.f;
+  }
+  __syncthreads();
+  float m[8], l[8], acc[8][CPL];
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[h][i] = 0.f;
+  }
+  const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)page_stride(D);
+  const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)slot_stride(D);
+  auto deq = [](const uint8_t* blk, int c, int bits) {
+    const uint32_t code = (blk[c * bits / 8] >> ((c * bits) & 7)) & ((1u << bits) - 1);
+    const __half2 pz = *reinterpret_cast<const __half2*>(blk + D * bits / 8 + 4 * (c / G));
+    return fmaf((float)code, __low2float(pz), __high2float(pz));
+  };
+  for (int t = u.tlo + warp; t < u.thi; t += NW) {
+    const bool is2 = t < u.npg;
+    const int nrow = is2 ? G : min(32, u.n4 - 32 * (t - u.npg));
+    for (int r = 0; r < nrow; ++r) {
+      float kx[CPL], vx[CPL];
+      if (is2) {
+        const uint8_t* rec = kv2 + (int64_t)a.page_ids[u.pg0 + t] * page_stride(D);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          const int c = lane + 32 * i;
+          const uint32_t code = (rec[8 * c + r / 4] >> (2 * (r & 3))) & 3u;
+          const __half2 pz = *reinterpret_cast<const __half2*>(rec + 8 * D + 4 * c);
+          kx[i] = fmaf((float)code, __low2float(pz), __high2float(pz));
+          vx[i] = deq(rec + key_page_bytes(D) + r * tok_bytes(D, 2), c, 2);
+        }
+      } else {
+        const int64_t slot = a.int4_ids[u.i40 + 32 * (t - u.npg) + r];
+        const uint8_t* rec = kv4 + slot * slot_stride(D);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          const int c = lane + 32 * i;
+          kx[i] = deq(rec, c, 4);
+          vx[i] = deq(rec + tok_bytes(D, 4), c, 4);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        if (h >= a.gq) continue;
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) s = fmaf(qs[h][lane + 32 * i], kx[i], s);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        const float mn = fmaxf(m[h], s);
+        const float al = exp2f(m[h] - mn), pv = exp2f(s - mn);
+        m[h] = mn;
+        l[h] = l[h] * al + pv;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[h][i] = fmaf(acc[h][i], al, pv * vx[i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 8; ++h) {
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) sm_acc[(warp * 8 + h) * D + lane + 32 * i] = acc[h][i];
+    if (lane == 0) {
+      sm_m[warp * 8 + h] = m[h];
+      sm_l[warp * 8 + h] = l[h];
+    }
+  }
+  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc);
+}
+
+// ====================================================================================
+// K3: merge the partials of each (request, q head) -> out.  attention.py:154-165.
+template <int D>
+__global__ void combine_kernel(const DecodeArgs a) {
+  const int bh = blockIdx.x;
+  const int b = bh / a.n_q, hq = bh % a.n_q;
+  const int kvh = hq / a.gq, hh = hq % a.gq;
+  const int unit = b * a.n_kv + kvh;
+  const int p0 = a.part_indptr[unit], p1 = a.part_indptr[unit + 1];
+  float M = -INFINITY;
+  for (int p = p0; p < p1; ++p) M = fmaxf(M, a.ws[((int64_t)p * a.gq + hh) * (D + 2) + D]);
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    float acc = 0.f, l = 0.f;
+    for (int p = p0; p < p1; ++p) {
+      const float* src = a.ws + ((int64_t)p * a.gq + hh) * (D + 2);
+      const float f = src[D] == -INFINITY ? 0.f : exp2f(src[D] - M);
+      acc = fmaf(src[c], f, acc);
+      l = fmaf(src[D + 1], f, l);
+    }
+    const float v = acc / l;
+    const int64_t oi = ((int64_t)b * a.n_q + hq) * D + c;
+    if (a.out_dtype == KVMIX_F32) reinterpret_cast<float*>(a.out)[oi] = v;
+    else if (a.out_dtype == KVMIX_BF16) reinterpret_cast<__nv_bfloat16*>(a.out)[oi] = __float2bfloat16(v);
+    else reinterpret_cast<__half*>(a.out)[oi] = __float2half(v);
+  }
+}
+
+template <int D>
+static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaStream_t s) {
+  if (variant == 0) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           Cfg<D>::SMEM);
+      if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
+      attr_set = true;
+    }
+    decode_mma_kernel<D><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
+  } else {
+    decode_simple_kernel<D><<<(unsigned)n_work, NW * 32, 0, s>>>(a);
+  }
+  int rc = check_launch("flash_decode");
+  if (rc) return rc;
+  combine_kernel<D><<<(unsigned)(a.batch * a.n_q), D, 0, s>>>(a);
+  return check_launch("flash_decode_combine");
+}
+
+// merge_partials (attention.py:154-165) for host-supplied partials, natural-log domain.
+__global__ void merge_partials_kernel(const float* __restrict__ acc, const float* __restrict__ lse,
+                                      const float* __restrict__ mx, int64_t n, int64_t d, float* __restrict__ out) {
+  float M = -INFINITY;
+  for (int64_t i = 0; i < n; ++i) M = fmaxf(M, mx[i]);
+  float z = 0.f;
+  for (int64_t i = 0; i < n; ++i) z += expf(lse[i] - M);
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    float a = 0.f;
+    for (int64_t i = 0; i < n; ++i) a += acc[i * d + c] * expf(mx[i] - M);
+    out[c] = a / z;
+  }
+}
+
+}  // namespace kvmix
+
+using namespace kvmix;
+
+extern "C" int kvmix_merge_partials(const float* acc, const float* lse, const float* mx, int64_t n, int64_t d,
+                                    float* out, void* stream) {
+  if (n <= 0) return fail(KVMIX_EINVAL, "cannot merge an empty partial list");
+  merge_partials_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(acc, lse, mx, n, d, out);
+  return check_launch("merge_partials");
+}
+
+extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
+                                  const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
+                                  int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
+                                  int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
+                                  const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
+                                  int64_t n_work, const int32_t* part_indptr, float* workspace,
+                                  int64_t workspace_floats, float scale, int32_t variant, void* stream) {
+  if (n_kv <= 0 || n_q % n_kv) return fail(KVMIX_EINVAL, "n_heads not a multiple of the pool's n_kv_heads");
+  const int64_t gq = n_q / n_kv;
+  if (gq > 8) return fail(KVMIX_EINVAL, "GQA group > 8 not supported");
+  if (batch <= 0 || n_work <= 0) return fail(KVMIX_EINVAL, "empty batch or work list");
+  if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
+  if (variant != 0 && variant != 1) return fail(KVMIX_EINVAL, "bad variant");
+  (void)workspace_floats;
+  DecodeArgs a;
+  a.q = q;
+  a.q_dtype = q_dtype;
+  a.out = out;
+  a.out_dtype = out_dtype;
+  a.int2_pool = int2_pool;
+  a.int4_pool = int4_pool;
+  a.pool_pages = pool_pages;
+  a.pool_int4 = pool_int4;
+  a.layer = layer;
+  a.n_kv = (int)n_kv;
+  a.n_q = (int)n_q;
+  a.gq = (int)gq;
+  a.batch = (int)batch;
+  a.page_indptr = page_indptr;
+  a.page_ids = page_ids;
+  a.int4_indptr = int4_indptr;
+  a.int4_ids = int4_ids;
+  a.work = work;
+  a.part_indptr = part_indptr;
+  a.ws = workspace;
+  a.qscale = scale * LOG2E;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (d) {
+    case 32: return launch_decode<32>(a, n_work, variant, s);
+    case 64: return launch_decode<64>(a, n_work, variant, s);
+    case 128: return launch_decode<128>(a, n_work, variant, s);
+    default: return fail(KVMIX_EINVAL, "decode supports head_dim 32, 64, 128");
+  }
+}
