@@ -1,0 +1,445 @@
+"""Benchmark: mixed INT2/INT4 split-K decode attention over the paged pool on B200.
+
+Default workload (BASELINE.json configs[1], "cfg2"): Qwen3-VL-32B-shaped decode --
+64 layers, 64 q / 8 kv heads, head_dim 128, batch 16, 32K-token tagged KV caches
+(per-token bits from bench_data/tagged_bits.npz, produced by the reference's host
+tagger/calibration/allocator at B=2.5), 1 GPU.  One step = one decode step's attention
+over all 64 layers: per layer the K2 split-decode kernel + the K3 combine kernel.
+Metric: decode tokens/s (= batch / step time) with HBM GB/s fraction of the K2 kernel.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun: batch-parallel (weak scaling), every rank owns a full pool
+and its own 16 requests; no collective on the data path.  Timing: CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks.  Per-layer KV
+(~0.5 GB) exceeds the 126 MB L2, so no L2 flush is needed between steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "mixed INT2/INT4 decode-attn tokens/s & HBM GB/s frac (Qwen3-VL-32B shape, 32K)"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--layers", type=int, default=64)
+    ap.add_argument("--q-heads", type=int, default=64)
+    ap.add_argument("--kv-heads", type=int, default=8)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-units", type=int, default=0, help="(request, layer) units timed on CPU")
+    ap.add_argument("--profile-only", action="store_true", help="build + a few steps, no JSON (for ncu)")
+    return ap.parse_args()
+
+
+def tagged_bits(n_req: int, ctx: int, seed_offset: int = 0) -> list[np.ndarray]:
+    """Per-request bit maps: the reference-tagged maps when available for this context,
+    else i.i.d. bits with the same INT2 fraction (0.8285)."""
+    path = os.path.join(ROOT, "bench_data", "tagged_bits.npz")
+    key = f"bits_{ctx}"
+    out = []
+    data = np.load(path) if os.path.exists(path) else {}
+    if key in data:
+        packed = data[key]
+        for r in range(n_req):
+            row = np.unpackbits(packed[(r + seed_offset) % packed.shape[0]])[:ctx]
+            out.append(np.where(row == 1, 2, 4).astype(np.int8))
+    else:
+        rng = np.random.default_rng(20261017 + seed_offset)
+        for _ in range(n_req):
+            out.append(np.where(rng.random(ctx) < 0.8285, 2, 4).astype(np.int8))
+    return out
+
+
+def algorithmic_bytes_per_layer(batch_obj, n_q_heads, head_dim) -> int:
+    """KV payload bytes + q + o (bf16) + page-table ints."""
+    t = batch_obj.csr
+    kv = batch_obj.kv_bytes()
+    qo = 2 * batch_obj.batch * n_q_heads * head_dim * 2
+    tables = 4 * int(t["n_pages"].sum() + t["n_int4"].sum())
+    return int(kv + qo + tables)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------
+# CPU baseline: the oracle port (numpy restatement of the reference flash_decode,
+# attention.py:175-218) on host cores; one worker per core over (request, layer) units.
+def _cpu_unit(args):
+    ctx, hkv, hq, d, seed = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import attention as oatt
+    from oracle import pool as opool
+    rng = np.random.default_rng(seed)
+    bits = tagged_bits(1, ctx, seed_offset=seed)[0]
+    k = (rng.standard_normal((1, ctx, hkv, d), dtype=np.float32)
+         * np.exp(rng.uniform(np.log(0.5), np.log(4.0), (hkv, d))).astype(np.float32))
+    v = rng.standard_normal((1, ctx, hkv, d), dtype=np.float32)
+    q = rng.standard_normal((hq, d), dtype=np.float32)
+    n2 = int((bits == 2).sum()) // 32 * 32
+    cfg = opool.Config(total_slots=ctx + 32, offset=n2, n_layers=1, n_kv_heads=hkv, head_dim=d)
+    op = opool.OraclePool(cfg)
+    op.alloc("r", bits)
+    op.write_prefill("r", k, v)
+    op.partition("r")
+    t0 = time.perf_counter()
+    oatt.flash_decode_pool(q, op, "r", 0)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(args, n_units: int, workers: int) -> dict:
+    ctx_cpu = args.ctx
+    jobs = [(ctx_cpu, args.kv_heads, args.q_heads, args.head_dim, 1000 + i) for i in range(n_units)]
+    ctx_mp = mp.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx_mp.Pool(workers) as p:
+        times = p.map(_cpu_unit, jobs)
+    wall = time.perf_counter() - t0
+    per_unit = float(np.mean(times))
+    units_per_step = args.batch * args.layers
+    # all cores busy on independent (request, layer) units
+    step_s = per_unit * units_per_step / workers
+    return {
+        "value": args.batch / step_s,
+        "unit": UNIT,
+        "cores": workers,
+        "kind": "port",
+        "sample": (f"{n_units} (request, layer) flash_decode units at {ctx_cpu} tokens, "
+                   f"{args.q_heads}/{args.kv_heads} heads, d={args.head_dim} (oracle restatement of "
+                   f"attention.py:175-218); mean {per_unit:.3f} s/unit, extrapolated to "
+                   f"{units_per_step} units/step over {workers} workers; sample wall {wall:.1f} s"),
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    n_units = max(workers, args.cpu_sample_units or workers)
+    per_step = []
+    res = None
+    for _ in range(max(1, args.steps if args.steps <= 2 else 1)):
+        res = cpu_baseline(args, n_units, workers)
+        per_step.append(res["value"])
+    value = res["value"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.batch / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference-tagged per-token bits, random K/V)",
+        "config": {"workload": "cfg2 decode attention: 64L, 64q/8kv heads, d128, batch 16, 32K ctx",
+                   "batch": args.batch, "ctx": args.ctx, "layers": args.layers},
+        "cpu_baseline": {"kind": res["kind"], "cores": res["cores"], "sample": res["sample"], "value": value,
+                         "unit": UNIT},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------
+def build_workload(args, device, rank: int):
+    import torch
+
+    import paper_2605_17170_b200 as kv
+
+    L, H, Hq, d, B, N = args.layers, args.kv_heads, args.q_heads, args.head_dim, args.batch, args.ctx
+    bits = tagged_bits(B, N, seed_offset=rank * B)
+    g = 32
+    n_pages = [int((b == 2).sum()) // g for b in bits]
+    n_int4 = [N - p * g for p in n_pages]
+    decode_room = 64 * B
+    cfg = kv.PoolConfig(total_slots=sum(n_pages) * g + sum(n_int4) + decode_room, offset=sum(n_pages) * g,
+                        n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg, device=device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(20261017 + rank)
+    ch_scale = torch.exp(torch.empty((H, d), device=device).uniform_(math.log(0.5), math.log(4.0), generator=gen))
+    rids = []
+    lchunk = 8  # layers per prefill call keeps the bf16 K/V staging at ~1 GB
+    for r in range(B):
+        rid = f"req{r}"
+        table = pool.alloc(rid, bits[r])
+        for l0 in range(0, L, lchunk):
+            nl = min(lchunk, L - l0)
+            k = (torch.randn((nl, N, H, d), device=device, generator=gen) * ch_scale).to(torch.bfloat16)
+            v = torch.randn((nl, N, H, d), device=device, generator=gen).to(torch.bfloat16)
+            _prefill_layers(pool, table, k, v, l0)
+            del k, v
+        pool.partition(table)
+        rids.append(rid)
+    torch.cuda.synchronize()
+    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq)
+    q = torch.randn((L, B, Hq, d), device=device, generator=gen).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    return pool, batch, q, out, bits
+
+
+def _prefill_layers(pool, table, k, v, l0):
+    """write_prefill for a layer slice (the pool API writes all layers; the bench streams
+    8 layers at a time to bound the staging memory) via the same C-ABI entry point."""
+    import torch
+
+    from paper_2605_17170_b200 import _lib
+    cfg, g = pool.config, pool.config.page_size
+    s = table.slots
+    is2 = s < cfg.offset
+    t2 = np.flatnonzero(is2)
+    t4 = np.flatnonzero(~is2)
+    pt = torch.as_tensor(t2.reshape(-1, g).astype(np.int32), device=pool.device)
+    pi = torch.as_tensor((s[t2[::g]] // g).astype(np.int32), device=pool.device)
+    it = torch.as_tensor(t4.astype(np.int32), device=pool.device)
+    ii = torch.as_tensor((s[t4] - cfg.offset).astype(np.int32), device=pool.device)
+    lh = l0 * cfg.n_kv_heads
+    _lib.check(_lib.lib.kvmix_write_prefill(
+        k.data_ptr(), v.data_ptr(), _lib.dtype_code(k), k.shape[0], k.shape[1], cfg.n_kv_heads, cfg.head_dim,
+        pt.data_ptr(), pi.data_ptr(), pt.shape[0], it.data_ptr(), ii.data_ptr(), t4.size,
+        pool.int2_pool.data_ptr() + lh * pool.n_pages * pool.page_stride, pool.n_pages,
+        pool.int4_pool.data_ptr() + lh * pool.n_int4 * pool.slot_stride, pool.n_int4, None, _lib.stream()))
+    pool._page_written[l0:l0 + k.shape[0], :, s[t2[::g]] // g] = True
+    pool._int4_written[l0:l0 + k.shape[0], :, s[t4] - cfg.offset] = True
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_17170_b200 as kv
+    from paper_2605_17170_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    pool, batch, q, out, bits = build_workload(args, device, rank)
+    L = args.layers
+    stream = torch.cuda.current_stream()
+
+    def step(variant=args.variant, partials_only=False):
+        v = variant | (0x100 if partials_only else 0)
+        for layer in range(L):
+            kv.flash_decode_batched(q[layer], batch, layer, out=out[layer], variant=v)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    # capture one step (64 x (K2 + K3)) in a CUDA graph; replays are the timed region
+    graph = torch.cuda.CUDAGraph()
+    s_cap = torch.cuda.Stream()
+    s_cap.wait_stream(stream)
+    with torch.cuda.stream(s_cap):
+        step()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s_cap):
+            step()
+    stream.wait_stream(s_cap)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    if args.profile_only:
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        return
+
+    def timed(fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        if world > 1:
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    with ClockSampler(local) as clocks:
+        ms_step = timed(graph.replay, args.steps)
+    # K2 alone (partials only), same launches, for the roofline of the dominant kernel
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s_cap):
+        with torch.cuda.graph(g2, stream=s_cap):
+            step(partials_only=True)
+    torch.cuda.synchronize()
+    g2.replay()
+    ms_k2_step = timed(g2.replay, args.steps)
+    ms_k2 = ms_k2_step / L
+
+    # end to end through the public API: pinned host q in, host out back, every step
+    e2e = None
+    if not args.no_e2e:
+        q_host = q.cpu().pin_memory()
+        o_host = torch.empty_like(q_host).pin_memory()
+        q_dev = torch.empty_like(q)
+        o_dev = torch.empty_like(q)
+
+        def e2e_step():
+            q_dev.copy_(q_host, non_blocking=True)
+            for layer in range(L):
+                kv.flash_decode_batched(q_dev[layer], batch, layer, out=o_dev[layer])
+            o_host.copy_(o_dev, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        ms_e2e = timed(e2e_step, max(3, args.steps // 2))
+        nbytes = q_host.numel() * q_host.element_size()
+        e2e = {"value": world * args.batch / (ms_e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "ms_per_step": ms_e2e}
+
+    # parity spot check of this run's first request/layer against the slow CUDA-core variant
+    ref_out = torch.empty_like(out[0])
+    kv.flash_decode_batched(q[0], batch, 0, out=ref_out, variant=1)
+    step()
+    torch.cuda.synchronize()
+    parity = float((out[0].float() - ref_out.float()).abs().max().item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    alg_bytes = algorithmic_bytes_per_layer(batch, args.q_heads, args.head_dim)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak = json.load(open(peaks_path))["hbm_gbs"]
+        peak_src = "measured"
+    else:
+        peak, peak_src = 6650.0, "fallback"
+    achieved = alg_bytes / (ms_k2 / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+    n2 = int(batch.csr["n_pages"].sum()) * 32
+    ntok = int(batch.n_tokens.sum())
+    value = world * args.batch / (ms_step / 1000.0)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int2/int4 KV, fp16 MMA, fp32 accumulate (bf16 q/o)",
+        "data": "synthetic: reference-tagged per-token bits (B=2.5), random bf16 K/V and q",
+        "config": {"workload": "cfg2 decode attention: 64 layers, 64q/8kv heads, d=128, batch 16, 32K ctx",
+                   "layers": args.layers, "batch_per_gpu": args.batch, "ctx": args.ctx,
+                   "q_heads": args.q_heads, "kv_heads": args.kv_heads, "head_dim": args.head_dim,
+                   "parallelism": f"batch-parallel x{world}", "stored_int2_fraction": n2 / ntok,
+                   "l2": "inputs larger than L2 (0.46 GB KV per layer)", "work_items_per_layer": batch.n_work},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": "decode_mma_kernel (K2)",
+                     "algorithmic_bytes_per_launch": alg_bytes, "k2_ms_per_launch": ms_k2},
+        "e2e": e2e,
+        "gpu_launches": args.steps * L * 2,
+        "clocks": clocks.summary(),
+        "parity_vs_cuda_core_variant_max_abs": parity,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        workers = os.cpu_count() or 1
+        line["cpu_baseline"] = cpu_baseline(args, max(workers, args.cpu_sample_units or workers), workers)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import __graft_entry__
+    __graft_entry__.build()
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -245,12 +245,12 @@ class OraclePool:
             row = slots[is2] % g
             if not self.page_written[layer][:, pg].all():
                 raise OracleError("validation", "slot read before write")
-            rec = self.int2[layer][:, pg]  # [H, m2, stride]
-            kd = codec.decode_key_pages(rec[..., :self.kp], d, g)  # [H, m2, G, d]
-            k[is2] = np.swapaxes(np.take_along_axis(kd, row[None, :, None, None], axis=2)[:, :, 0], 0, 1)
+            upg, inv = np.unique(pg, return_inverse=True)  # decode each page once (pool.py:419-425)
+            rec = self.int2[layer][:, upg]  # [H, P, stride]
+            kd = codec.decode_key_pages(rec[..., :self.kp], d, g)  # [H, P, G, d]
+            k[is2] = np.swapaxes(kd[:, inv, row], 0, 1)
             vrec = rec[..., self.kp:self.kp + g * self.tb2].reshape(H, -1, g, self.tb2)
-            vsel = np.take_along_axis(vrec, row[None, :, None, None], axis=2)[:, :, 0]
-            v[is2] = np.swapaxes(codec.decode_token_blocks(vsel, d, 2, g), 0, 1)
+            v[is2] = np.swapaxes(codec.decode_token_blocks(vrec[:, inv, row], d, 2, g), 0, 1)
         if (~is2).any():
             idx = slots[~is2] - off
             if not self.slot_written[layer][:, idx].all():

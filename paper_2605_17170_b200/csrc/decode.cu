@@ -25,7 +25,7 @@
 namespace kvmix {
 
 constexpr int NW = 4;      // warps per CTA
-constexpr int STAGES = 4;  // ring depth per warp
+constexpr int STAGES = 3;  // ring depth per warp
 constexpr uint32_t MAGIC = 0x3C003C00u;
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -137,9 +137,221 @@ __device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit&
 }
 
 // ====================================================================================
-// Variant 0: tensor-core kernel.
+// Variant 0: tensor-core kernel.  Tile bodies are specialised per bitwidth so that all
+// shared-memory addresses are a lane-constant base plus compile-time immediates.
+struct Softmax {
+  float m0, m1, l0, l1;  // running max / sum for heads 2q, 2q+1 (log2 domain)
+};
+
 template <int D>
-__global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs a) {
+struct Acc {
+  float o[D / 16][4];   // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
+  float zs[D / 32][4];  // sum_t p * z per channel group
+  uint32_t one[4];      // A operand of all-ones (fp16 1.0) kept in one register quad
+};
+
+__device__ __forceinline__ uint32_t ld_s32(const uint8_t* base, int off) {
+  return *reinterpret_cast<const uint32_t*>(base + off);
+}
+
+// Online softmax over one 32-token tile; returns the P^T B fragments of PV k-steps 0, 1.
+template <int D>
+__device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, Acc<D>& acc, uint32_t (&bP)[2][2]) {
+  float tm0 = fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6]));
+  float tm1 = fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7]));
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
+    tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
+  }
+  const float mn0 = fmaxf(st.m0, tm0), mn1 = fmaxf(st.m1, tm1);
+  if (__any_sync(0xffffffffu, (mn0 != st.m0) || (mn1 != st.m1))) {
+    const float al0 = fast_exp2(st.m0 - mn0), al1 = fast_exp2(st.m1 - mn1);  // exp2(-inf) = 0
+    st.l0 *= al0;
+    st.l1 *= al1;
+#pragma unroll
+    for (int m = 0; m < D / 16; ++m) {
+      acc.o[m][0] *= al0; acc.o[m][2] *= al0;
+      acc.o[m][1] *= al1; acc.o[m][3] *= al1;
+    }
+#pragma unroll
+    for (int j = 0; j < D / 32; ++j) {
+      acc.zs[j][0] *= al0; acc.zs[j][2] *= al0;
+      acc.zs[j][1] *= al1; acc.zs[j][3] *= al1;
+    }
+    st.m0 = mn0;
+    st.m1 = mn1;
+  }
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) {
+    p[i] = fast_exp2(sv[i] - mn0);
+    p[i + 1] = fast_exp2(sv[i + 1] - mn1);
+  }
+  st.l0 += (p[0] + p[2]) + (p[4] + p[6]);
+  st.l1 += (p[1] + p[3]) + (p[5] + p[7]);
+  // k index of PV == QK row: lane holds head g, rows (2q, 2q+1) / (2q+8, 2q+9)
+  bP[0][0] = movtrans(pack_h2(p[0], p[1]));
+  bP[0][1] = movtrans(pack_h2(p[2], p[3]));
+  bP[1][0] = movtrans(pack_h2(p[4], p[5]));
+  bP[1][1] = movtrans(pack_h2(p[6], p[7]));
+}
+
+// PV for one k-step and one channel group j: A = code fields of the pair-A / pair-B
+// tokens (rows e = 0..3 -> channels 32j + 4g + e), B = P' = p*s and P*z.
+template <int D>
+__device__ __forceinline__ void pv_group(Acc<D>& acc, int j, const uint32_t (&fA)[4], const uint32_t (&fB)[4],
+                                         uint32_t bP0, uint32_t bP1, uint32_t pA0, uint32_t pA1, uint32_t pB0,
+                                         uint32_t pB1) {
+  const uint64_t ps = pack_b64(hmul2u(bP0, prmt(pA0, pA1, 0x5410)), hmul2u(bP1, prmt(pB0, pB1, 0x5410)));
+  const uint64_t pz = pack_b64(hmul2u(bP0, prmt(pA0, pA1, 0x7632)), hmul2u(bP1, prmt(pB0, pB1, 0x7632)));
+  mma16816_b64(acc.o[2 * j], fA[0], fA[1], fB[0], fB[1], ps);
+  mma16816_b64(acc.o[2 * j + 1], fA[2], fA[3], fB[2], fB[3], ps);
+  mma16816_b64(acc.zs[j], acc.one[0], acc.one[1], acc.one[2], acc.one[3], pz);  // sum_t p*z
+}
+
+// ---------------------------------- INT2 page tile ----------------------------------
+template <int D>
+__device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const uint64_t (&qb2)[D / 16],
+                                          int lane, Softmax& st, Acc<D>& acc) {
+  using C = Cfg<D>;
+  const int g = lane >> 2, q = lane & 3;
+  // lane g reads byte beta(g) = (g>>1) | ((g&1)<<2) of every channel word -> tokens 4beta..4beta+3
+  const uint32_t selK = (uint32_t)(g >> 1) | ((uint32_t)(4 + (g >> 1)) << 8);
+  const uint8_t* kb = buf + 16 * q + 4 * (g & 1);  // + 128 i (+8 second channel, +64 / +72 channel+8)
+  const uint8_t* pb = buf + 8 * D + 8 * q;          // params of channel 16i+2q: + 64 i (+32 for +8)
+  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < C::NCH; ++i) {
+    const uint32_t r1 = prmt(ld_s32(kb, 128 * i), ld_s32(kb, 128 * i + 8), selK);
+    const uint32_t r2 = prmt(ld_s32(kb, 128 * i + 64), ld_s32(kb, 128 * i + 72), selK);
+    const uint2 p1 = *reinterpret_cast<const uint2*>(pb + 64 * i);
+    const uint2 p2 = *reinterpret_cast<const uint2*>(pb + 64 * i + 32);
+    const uint64_t qs = pack_b64(hmul2u(lo32(qb2[i]), prmt(p1.x, p1.y, 0x5410)),
+                                 hmul2u(hi32(qb2[i]), prmt(p2.x, p2.y, 0x5410)));
+    const uint32_t z1 = prmt(p1.x, p1.y, 0x7632), z2 = prmt(p2.x, p2.y, 0x7632);
+    mma16816_b64(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qs);
+    mma16816_b64(c1, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qs);
+    // bias rows g carry sum_c q_c z_c; rows g+8 (cb[2], cb[3]) are don't-care filler
+    mma16816_b64(cb, z1, r1, z2, r2, qb2[i]);
+  }
+  // undo 2^(2k-10) per token row (k = token position inside its code byte)
+  const float sv[8] = {fmaf(c0[0], 1024.f, cb[0]), fmaf(c0[1], 1024.f, cb[1]), fmaf(c0[2], 256.f, cb[0]),
+                       fmaf(c0[3], 256.f, cb[1]),  fmaf(c1[0], 64.f, cb[0]),   fmaf(c1[1], 64.f, cb[1]),
+                       fmaf(c1[2], 16.f, cb[0]),   fmaf(c1[3], 16.f, cb[1])};
+  uint32_t bP[2][2];
+  softmax_tile<D>(sv, st, acc, bP);
+  // PV: k-step ks, pair A tokens (4q+2ks, 16+4q+2ks), pair B = pair A + 1
+  const uint32_t selV = (uint32_t)(g & 3) | ((uint32_t)(4 + (g & 3)) << 8);
+  const uint8_t* vb = buf + C::KP + C::TB2 * 4 * q;  // token 4q's V block
+  const uint8_t* vc = vb + 4 * (g >> 2);             // + 8j: word of byte 8j+g
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    constexpr int T = C::TB2;
+    uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
+    lds_params<C::NGRP>(vb + (2 * ks) * T + D / 4, pA0);
+    lds_params<C::NGRP>(vb + (16 + 2 * ks) * T + D / 4, pA1);
+    lds_params<C::NGRP>(vb + (2 * ks + 1) * T + D / 4, pB0);
+    lds_params<C::NGRP>(vb + (17 + 2 * ks) * T + D / 4, pB1);
+#pragma unroll
+    for (int j = 0; j < C::NGRP; ++j) {
+      const uint32_t rA = prmt(ld_s32(vc, (2 * ks) * T + 8 * j), ld_s32(vc, (16 + 2 * ks) * T + 8 * j), selV);
+      const uint32_t rB = prmt(ld_s32(vc, (2 * ks + 1) * T + 8 * j), ld_s32(vc, (17 + 2 * ks) * T + 8 * j), selV);
+      uint32_t fA[4], fB[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        fA[e] = int2_field(rA, e);
+        fB[e] = int2_field(rB, e);
+      }
+      pv_group<D>(acc, j, fA, fB, bP[ks][0], bP[ks][1], pA0[j], pA1[j], pB0[j], pB1[j]);
+    }
+  }
+}
+
+// ---------------------------------- INT4 slot tile ----------------------------------
+__device__ __forceinline__ uint32_t int4_deq(uint32_t field16, uint32_t s16, uint32_t zz) {
+  return hfma2u(hsub2u(field16, MAGIC), s16, zz);  // (code/16) * 16s + z
+}
+
+template <int D, bool FULL>
+__device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const uint64_t (&qb4)[D / 16],
+                                          int lane, Softmax& st, Acc<D>& acc) {
+  using C = Cfg<D>;
+  constexpr int S = C::SSM;
+  const int g = lane >> 2, q = lane & 3;
+  const uint8_t* kb = buf + S * g + 4 * q;  // slot row r: + S*(16(r>>1) + 8(r&1)); group j: + 16j
+  const uint8_t* kp = buf + S * g + D / 2;  // K params of the slot: + 4j
+  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < C::NGRP; ++j) {
+    uint32_t e[4][4];  // [slot row: M0 g, M0 g+8, M1 g, M1 g+8][field]
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int ro = S * (16 * (r >> 1) + 8 * (r & 1));
+      const uint32_t w = ld_s32(kb, ro + 16 * j);
+      const uint32_t par = ld_s32(kp, ro + 4 * j);
+      const uint32_t s16 = hmul2u(prmt(par, par, 0x1010), 0x4C004C00u);  // (16s, 16s)
+      const uint32_t zz = prmt(par, par, 0x3232);
+      e[r][0] = int4_deq(lop_and_or(w << 6, 0x03C003C0u, MAGIC), s16, zz);
+      e[r][1] = int4_deq(lop_and_or(w << 2, 0x03C003C0u, MAGIC), s16, zz);
+      e[r][2] = int4_deq(lop_and_or(w >> 2, 0x03C003C0u, MAGIC), s16, zz);
+      e[r][3] = int4_deq(lop_and_or(w >> 6, 0x03C003C0u, MAGIC), s16, zz);
+    }
+    mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], qb4[2 * j]);
+    mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], qb4[2 * j + 1]);
+    mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], qb4[2 * j]);
+    mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], qb4[2 * j + 1]);
+  }
+  float sv[8] = {c0[0], c0[1], c0[2], c0[3], c1[0], c1[1], c1[2], c1[3]};
+  if (!FULL) {
+    if (g >= nv) sv[0] = sv[1] = -INFINITY;
+    if (g + 8 >= nv) sv[2] = sv[3] = -INFINITY;
+    if (g + 16 >= nv) sv[4] = sv[5] = -INFINITY;
+    if (g + 24 >= nv) sv[6] = sv[7] = -INFINITY;
+  }
+  uint32_t bP[2][2];
+  softmax_tile<D>(sv, st, acc, bP);
+  const uint32_t b4 = 2 * (g & 1);
+  const uint32_t selV = b4 | ((b4 + 1) << 4) | ((b4 + 4) << 8) | ((b4 + 5) << 12);
+  const uint8_t* vb = buf + S * 2 * q + C::TB4;  // slot 2q's V block: + S*(16ks [+1] [+8])
+  const uint8_t* vc = vb + 4 * (g >> 1);         // + 16j: word holding bytes 16j+2g, +1
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
+    lds_params<C::NGRP>(vb + S * (16 * ks) + D / 2, pA0);
+    lds_params<C::NGRP>(vb + S * (16 * ks + 1) + D / 2, pA1);
+    lds_params<C::NGRP>(vb + S * (16 * ks + 8) + D / 2, pB0);
+    lds_params<C::NGRP>(vb + S * (16 * ks + 9) + D / 2, pB1);
+    if (!FULL) {
+      const int sA0 = 16 * ks + 2 * q;
+#pragma unroll
+      for (int j = 0; j < C::NGRP; ++j) {
+        if (sA0 >= nv) pA0[j] = 0u;
+        if (sA0 + 1 >= nv) pA1[j] = 0u;
+        if (sA0 + 8 >= nv) pB0[j] = 0u;
+        if (sA0 + 9 >= nv) pB1[j] = 0u;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < C::NGRP; ++j) {
+      const uint32_t rA = prmt(ld_s32(vc, S * (16 * ks) + 16 * j), ld_s32(vc, S * (16 * ks + 1) + 16 * j), selV);
+      const uint32_t rB = prmt(ld_s32(vc, S * (16 * ks + 8) + 16 * j), ld_s32(vc, S * (16 * ks + 9) + 16 * j), selV);
+      uint32_t fA[4], fB[4];
+      fA[0] = hsub2u(lop_and_or(rA, 0x000F000Fu, MAGIC), MAGIC);
+      fA[1] = hsub2u(lop_and_or(rA >> 2, 0x003C003Cu, MAGIC), MAGIC);
+      fA[2] = hsub2u(lop_and_or(rA >> 4, 0x00F000F0u, MAGIC), MAGIC);
+      fA[3] = hsub2u(lop_and_or(rA >> 6, 0x03C003C0u, MAGIC), MAGIC);
+      fB[0] = hsub2u(lop_and_or(rB, 0x000F000Fu, MAGIC), MAGIC);
+      fB[1] = hsub2u(lop_and_or(rB >> 2, 0x003C003Cu, MAGIC), MAGIC);
+      fB[2] = hsub2u(lop_and_or(rB >> 4, 0x00F000F0u, MAGIC), MAGIC);
+      fB[3] = hsub2u(lop_and_or(rB >> 6, 0x03C003C0u, MAGIC), MAGIC);
+      pv_group<D>(acc, j, fA, fB, bP[ks][0], bP[ks][1], pA0[j], pA1[j], pB0[j], pB1[j]);
+    }
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(NW * 32, 3) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[NW][STAGES];
@@ -158,7 +370,7 @@ __global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs
   // ---- Q fragments (B operand of QK), fp16, pre-scaled by scale*log2(e) ----
   // qb2: INT2 key pages, chunk i covers channels 16i..16i+15 in natural order.
   // qb4: INT4 keys, chunk 2j+s pairs channels (32j+8q+{0,4}/{1,5}) (s=0) or ({2,6}/{3,7}) (s=1).
-  uint32_t qb2[C::NCH][2], qb4[C::NCH][2];
+  uint64_t qb2[C::NCH], qb4[C::NCH];
   {
     const bool hv = g < a.gq;
     const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
@@ -166,15 +378,12 @@ __global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs
 #pragma unroll
     for (int i = 0; i < C::NCH; ++i) {
       const int c1 = 16 * i + 2 * q;
-      qb2[i][0] = pack_h2(qv(c1), qv(c1 + 1));
-      qb2[i][1] = pack_h2(qv(c1 + 8), qv(c1 + 9));
+      qb2[i] = pack_b64(pack_h2(qv(c1), qv(c1 + 1)), pack_h2(qv(c1 + 8), qv(c1 + 9)));
       const int base = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
-      qb4[i][0] = pack_h2(qv(base + 0), qv(base + 4));
-      qb4[i][1] = pack_h2(qv(base + 1), qv(base + 5));
+      qb4[i] = pack_b64(pack_h2(qv(base + 0), qv(base + 4)), pack_h2(qv(base + 1), qv(base + 5)));
     }
   }
 
-  // ---- tile enumeration for this warp ----
   const int ntiles = u.thi - u.tlo;
   const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
   const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
@@ -202,211 +411,29 @@ __global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs
       }
     }
   };
-
   for (int k = 0; k < STAGES && k < nmine; ++k) issue(k);
 
-  // ---- running state ----
-  float o[C::NCH][4];    // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
-  float zs[C::NGRP][4];  // sum_t p * z per channel group
+  Acc<D> acc;
 #pragma unroll
-  for (int m = 0; m < C::NCH; ++m) o[m][0] = o[m][1] = o[m][2] = o[m][3] = 0.f;
+  for (int i = 0; i < 4; ++i) asm volatile("mov.b32 %0, 0x3c003c00;" : "=r"(acc.one[i]));
 #pragma unroll
-  for (int j = 0; j < C::NGRP; ++j) zs[j][0] = zs[j][1] = zs[j][2] = zs[j][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
-  // INT2 page row map: lane g reads byte beta(g) of every channel word (tokens 4beta..4beta+3).
-  const uint32_t selK = (uint32_t)(g >> 1) | ((uint32_t)(4 + (g >> 1)) << 8);
-  const int koff = 4 * (g & 1);
-  const uint32_t selV2 = (uint32_t)(g & 3) | ((uint32_t)(4 + (g & 3)) << 8);
-  const int voff2 = 4 * (g >> 2);
-  const uint32_t b4 = 2 * (g & 1);
-  const uint32_t selV4 = b4 | ((b4 + 1) << 4) | ((b4 + 4) << 8) | ((b4 + 5) << 12);
-  const int voff4 = 4 * (g >> 1);
+  for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < C::NGRP; ++j) acc.zs[j][0] = acc.zs[j][1] = acc.zs[j][2] = acc.zs[j][3] = 0.f;
+  Softmax st{-INFINITY, -INFINITY, 0.f, 0.f};
 
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
     const int s = k % STAGES;
     const uint8_t* buf = ring + s * C::BUF;
     mbar_wait(&bars[warp][s], (uint32_t)((k / STAGES) & 1));
-
-    float sv[8];  // S (log2 domain) for rows {M0: g, g+8; M1: g, g+8} x heads {2q, 2q+1}
-    const bool is2 = t < u.npg;
-    int nv = 32;
-    // PV token pairs (smem offsets of the 4 token records of each k-step) and params
-    if (is2) {
-      // ---------------- QK over an INT2 key page ----------------
-      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1v[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
-      const uint8_t* kc = buf + koff;
-      const uint8_t* kpar = buf + 8 * D;
-#pragma unroll
-      for (int i = 0; i < C::NCH; ++i) {
-        const int ca = 16 * i + 2 * q, cc = ca + 8;
-        const uint32_t r1 = prmt(lds32(kc + 8 * ca), lds32(kc + 8 * ca + 8), selK);
-        const uint32_t r2 = prmt(lds32(kc + 8 * cc), lds32(kc + 8 * cc + 8), selK);
-        const uint2 p1 = *reinterpret_cast<const uint2*>(kpar + 4 * ca);
-        const uint2 p2 = *reinterpret_cast<const uint2*>(kpar + 4 * cc);
-        const uint32_t z1 = prmt(p1.x, p1.y, 0x7632), z2 = prmt(p2.x, p2.y, 0x7632);
-        const uint32_t qa = hmul2u(qb2[i][0], prmt(p1.x, p1.y, 0x5410));
-        const uint32_t qc = hmul2u(qb2[i][1], prmt(p2.x, p2.y, 0x5410));
-        mma16816(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qa, qc);
-        mma16816(c1v, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qa, qc);
-        mma16816(cb, z1, z1, z2, z2, qb2[i][0], qb2[i][1]);
-      }
-      // undo 2^(2k-10) per token row (k = position of the token inside its code byte)
-      sv[0] = fmaf(c0[0], 1024.f, cb[0]);
-      sv[1] = fmaf(c0[1], 1024.f, cb[1]);
-      sv[2] = fmaf(c0[2], 256.f, cb[0]);
-      sv[3] = fmaf(c0[3], 256.f, cb[1]);
-      sv[4] = fmaf(c1v[0], 64.f, cb[0]);
-      sv[5] = fmaf(c1v[1], 64.f, cb[1]);
-      sv[6] = fmaf(c1v[2], 16.f, cb[0]);
-      sv[7] = fmaf(c1v[3], 16.f, cb[1]);
+    if (t < u.npg) {
+      int2_tile<D>(buf, qb2, lane, st, acc);
     } else {
-      // ---------------- QK over INT4 keys (dequantised in registers) ----------------
-      nv = min(32, u.n4 - 32 * (t - u.npg));
-      float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1v[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int j = 0; j < C::NGRP; ++j) {
-        uint32_t e[4][4];  // [slot row: M0 g, M0 g+8, M1 g, M1 g+8][field]
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint8_t* rec = buf + C::SSM * (16 * (r >> 1) + g + 8 * (r & 1));
-          const uint32_t w = lds32(rec + 16 * j + 4 * q);
-          const uint32_t par = lds32(rec + D / 2 + 4 * j);
-          const uint32_t s16 = hmul2u(prmt(par, par, 0x1010), 0x4C004C00u);  // (16s, 16s)
-          const uint32_t zz = prmt(par, par, 0x3232);
-          e[r][0] = hfma2u(hsub2u(lop_and_or(w << 6, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
-          e[r][1] = hfma2u(hsub2u(lop_and_or(w << 2, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
-          e[r][2] = hfma2u(hsub2u(lop_and_or(w >> 2, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
-          e[r][3] = hfma2u(hsub2u(lop_and_or(w >> 6, 0x03C003C0u, MAGIC), MAGIC), s16, zz);
-        }
-        mma16816(c0, e[0][0], e[1][0], e[0][1], e[1][1], qb4[2 * j][0], qb4[2 * j][1]);
-        mma16816(c0, e[0][2], e[1][2], e[0][3], e[1][3], qb4[2 * j + 1][0], qb4[2 * j + 1][1]);
-        mma16816(c1v, e[2][0], e[3][0], e[2][1], e[3][1], qb4[2 * j][0], qb4[2 * j][1]);
-        mma16816(c1v, e[2][2], e[3][2], e[2][3], e[3][3], qb4[2 * j + 1][0], qb4[2 * j + 1][1]);
-      }
-      sv[0] = (g < nv) ? c0[0] : -INFINITY;
-      sv[1] = (g < nv) ? c0[1] : -INFINITY;
-      sv[2] = (g + 8 < nv) ? c0[2] : -INFINITY;
-      sv[3] = (g + 8 < nv) ? c0[3] : -INFINITY;
-      sv[4] = (g + 16 < nv) ? c1v[0] : -INFINITY;
-      sv[5] = (g + 16 < nv) ? c1v[1] : -INFINITY;
-      sv[6] = (g + 24 < nv) ? c1v[2] : -INFINITY;
-      sv[7] = (g + 24 < nv) ? c1v[3] : -INFINITY;
+      const int nv = min(32, u.n4 - 32 * (t - u.npg));
+      if (nv == 32) int4_tile<D, true>(buf, 32, qb4, lane, st, acc);
+      else int4_tile<D, false>(buf, nv, qb4, lane, st, acc);
     }
-
-    // ---------------- online softmax (log2 domain) ----------------
-    float tm0 = fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6]));
-    float tm1 = fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7]));
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
-      tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
-    }
-    const float mn0 = fmaxf(m0, tm0), mn1 = fmaxf(m1, tm1);
-    const float al0 = fast_exp2(m0 - mn0), al1 = fast_exp2(m1 - mn1);  // exp2(-inf) = 0
-    m0 = mn0;
-    m1 = mn1;
-    float p[8];
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-      p[i] = fast_exp2(sv[i] - mn0);
-      p[i + 1] = fast_exp2(sv[i + 1] - mn1);
-    }
-    l0 = l0 * al0 + (p[0] + p[2]) + (p[4] + p[6]);
-    l1 = l1 * al1 + (p[1] + p[3]) + (p[5] + p[7]);
-    if (__any_sync(0xffffffffu, (al0 != 1.f) || (al1 != 1.f))) {
-#pragma unroll
-      for (int m = 0; m < C::NCH; ++m) {
-        o[m][0] *= al0; o[m][2] *= al0;
-        o[m][1] *= al1; o[m][3] *= al1;
-      }
-#pragma unroll
-      for (int j = 0; j < C::NGRP; ++j) {
-        zs[j][0] *= al0; zs[j][2] *= al0;
-        zs[j][1] *= al1; zs[j][3] *= al1;
-      }
-    }
-    // P^T B fragments for PV k-steps 0, 1 (k index == QK row): lane holds head g,
-    // rows (2q, 2q+1) in bP[ks][0] and (2q+8, 2q+9) in bP[ks][1].
-    uint32_t bP[2][2];
-    bP[0][0] = movtrans(pack_h2(p[0], p[1]));
-    bP[0][1] = movtrans(pack_h2(p[2], p[3]));
-    bP[1][0] = movtrans(pack_h2(p[4], p[5]));
-    bP[1][1] = movtrans(pack_h2(p[6], p[7]));
-
-    // ---------------- PV ----------------
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      // smem records of the pair-A tokens (k = 2q, 2q+1) and pair-B tokens (2q+8, 2q+9)
-      const uint8_t *vA0, *vA1, *vB0, *vB1;
-      bool okA0 = true, okA1 = true, okB0 = true, okB1 = true;
-      if (is2) {
-        const int tA0 = 4 * q + 2 * ks, tA1 = 16 + 4 * q + 2 * ks;
-        const uint8_t* vb = buf + C::KP;
-        vA0 = vb + C::TB2 * tA0;
-        vA1 = vb + C::TB2 * tA1;
-        vB0 = vA0 + C::TB2;
-        vB1 = vA1 + C::TB2;
-      } else {
-        const int sA0 = 16 * ks + 2 * q;
-        vA0 = buf + C::SSM * sA0 + C::TB4;
-        vA1 = vA0 + C::SSM;
-        vB0 = vA0 + 8 * C::SSM;
-        vB1 = vB0 + C::SSM;
-        okA0 = sA0 < nv;
-        okA1 = sA0 + 1 < nv;
-        okB0 = sA0 + 8 < nv;
-        okB1 = sA0 + 9 < nv;
-      }
-      const int poff = is2 ? D / 4 : D / 2;
-      uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
-      lds_params<C::NGRP>(vA0 + poff, pA0);
-      lds_params<C::NGRP>(vA1 + poff, pA1);
-      lds_params<C::NGRP>(vB0 + poff, pB0);
-      lds_params<C::NGRP>(vB1 + poff, pB1);
-#pragma unroll
-      for (int j = 0; j < C::NGRP; ++j) {
-        if (!okA0) pA0[j] = 0u;
-        if (!okA1) pA1[j] = 0u;
-        if (!okB0) pB0[j] = 0u;
-        if (!okB1) pB1[j] = 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < C::NGRP; ++j) {
-        uint32_t rA, rB;
-        uint32_t fA[4], fB[4];
-        if (is2) {
-          rA = prmt(lds32(vA0 + 8 * j + voff2), lds32(vA1 + 8 * j + voff2), selV2);
-          rB = prmt(lds32(vB0 + 8 * j + voff2), lds32(vB1 + 8 * j + voff2), selV2);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            fA[e] = int2_field(rA, e);
-            fB[e] = int2_field(rB, e);
-          }
-        } else {
-          rA = prmt(lds32(vA0 + 16 * j + voff4), lds32(vA1 + 16 * j + voff4), selV4);
-          rB = prmt(lds32(vB0 + 16 * j + voff4), lds32(vB1 + 16 * j + voff4), selV4);
-          fA[0] = hsub2u(lop_and_or(rA, 0x000F000Fu, MAGIC), MAGIC);
-          fA[1] = hsub2u(lop_and_or(rA >> 2, 0x003C003Cu, MAGIC), MAGIC);
-          fA[2] = hsub2u(lop_and_or(rA >> 4, 0x00F000F0u, MAGIC), MAGIC);
-          fA[3] = hsub2u(lop_and_or(rA >> 6, 0x03C003C0u, MAGIC), MAGIC);
-          fB[0] = hsub2u(lop_and_or(rB, 0x000F000Fu, MAGIC), MAGIC);
-          fB[1] = hsub2u(lop_and_or(rB >> 2, 0x003C003Cu, MAGIC), MAGIC);
-          fB[2] = hsub2u(lop_and_or(rB >> 4, 0x00F000F0u, MAGIC), MAGIC);
-          fB[3] = hsub2u(lop_and_or(rB >> 6, 0x03C003C0u, MAGIC), MAGIC);
-        }
-        // P' = p * s (per token, group j) and P*z, as B fragments
-        const uint32_t sA = prmt(pA0[j], pA1[j], 0x5410), zA = prmt(pA0[j], pA1[j], 0x7632);
-        const uint32_t sB = prmt(pB0[j], pB1[j], 0x5410), zB = prmt(pB0[j], pB1[j], 0x7632);
-        const uint32_t ps0 = hmul2u(bP[ks][0], sA), ps1 = hmul2u(bP[ks][1], sB);
-        const uint32_t pz0 = hmul2u(bP[ks][0], zA), pz1 = hmul2u(bP[ks][1], zB);
-        mma16816(o[2 * j], fA[0], fA[1], fB[0], fB[1], ps0, ps1);
-        mma16816(o[2 * j + 1], fA[2], fA[3], fB[2], fB[3], ps0, ps1);
-        mma16816(zs[j], MAGIC, MAGIC, MAGIC, MAGIC, pz0, pz1);
-      }
-    }
-
     __syncwarp();
     if (k + STAGES < nmine) {
       fence_proxy_async();
@@ -417,8 +444,8 @@ __global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs
   // ---- finalize this warp: full l per head, acc[h][c] = 2^(10-2e) * O^T + zsum ----
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, off);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, off);
+    st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, off);
   }
   __syncthreads();  // all warps done with their rings -> reuse smem for the merge
   float* sm_acc = reinterpret_cast<float*>(smem);
@@ -430,16 +457,16 @@ __global__ void __launch_bounds__(NW * 32, 2) decode_mma_kernel(const DecodeArgs
     const int e0 = 2 * (m & 1);
     const int ch0 = 32 * j + 4 * g + e0;
     const float f0 = (float)(1 << (10 - 2 * e0)), f1 = (float)(1 << (10 - 2 * (e0 + 1)));
-    sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(o[m][0], f0, zs[j][0]);
-    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(o[m][1], f0, zs[j][1]);
-    sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(o[m][2], f1, zs[j][0]);
-    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(o[m][3], f1, zs[j][1]);
+    sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, acc.zs[j][0]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, acc.zs[j][1]);
+    sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, acc.zs[j][0]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(acc.o[m][3], f1, acc.zs[j][1]);
   }
   if (g == 0) {
-    sm_m[warp * 8 + 2 * q] = m0;
-    sm_m[warp * 8 + 2 * q + 1] = m1;
-    sm_l[warp * 8 + 2 * q] = l0;
-    sm_l[warp * 8 + 2 * q + 1] = l1;
+    sm_m[warp * 8 + 2 * q] = st.m0;
+    sm_m[warp * 8 + 2 * q + 1] = st.m1;
+    sm_l[warp * 8 + 2 * q] = st.l0;
+    sm_l[warp * 8 + 2 * q + 1] = st.l1;
   }
   merge_and_store<D>(a, u, sm_m, sm_l, sm_acc);
 }
@@ -557,7 +584,7 @@ __global__ void combine_kernel(const DecodeArgs a) {
 }
 
 template <int D>
-static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaStream_t s) {
+static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, bool partials_only, cudaStream_t s) {
   if (variant == 0) {
     static bool attr_set = false;
     if (!attr_set) {
@@ -571,7 +598,7 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
     decode_simple_kernel<D><<<(unsigned)n_work, NW * 32, 0, s>>>(a);
   }
   int rc = check_launch("flash_decode");
-  if (rc) return rc;
+  if (rc || partials_only) return rc;
   combine_kernel<D><<<(unsigned)(a.batch * a.n_q), D, 0, s>>>(a);
   return check_launch("flash_decode_combine");
 }
@@ -613,6 +640,8 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   if (gq > 8) return fail(KVMIX_EINVAL, "GQA group > 8 not supported");
   if (batch <= 0 || n_work <= 0) return fail(KVMIX_EINVAL, "empty batch or work list");
   if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
+  const bool partials_only = (variant & 0x100) != 0;  // measurement hook: skip K3
+  variant &= 0xff;
   if (variant != 0 && variant != 1) return fail(KVMIX_EINVAL, "bad variant");
   (void)workspace_floats;
   DecodeArgs a;
@@ -639,9 +668,9 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   a.qscale = scale * LOG2E;
   cudaStream_t s = (cudaStream_t)stream;
   switch (d) {
-    case 32: return launch_decode<32>(a, n_work, variant, s);
-    case 64: return launch_decode<64>(a, n_work, variant, s);
-    case 128: return launch_decode<128>(a, n_work, variant, s);
+    case 32: return launch_decode<32>(a, n_work, variant, partials_only, s);
+    case 64: return launch_decode<64>(a, n_work, variant, partials_only, s);
+    case 128: return launch_decode<128>(a, n_work, variant, partials_only, s);
     default: return fail(KVMIX_EINVAL, "decode supports head_dim 32, 64, 128");
   }
 }
