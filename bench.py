@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--kv-heads", type=int, default=8)
     ap.add_argument("--head-dim", type=int, default=128)
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--int2-frac", type=float, default=None, help="override: i.i.d. bits with this INT2 fraction")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-units", type=int, default=0, help="(request, layer) units timed on CPU")
@@ -223,6 +224,9 @@ def build_workload(args, device, rank: int):
 
     L, H, Hq, d, B, N = args.layers, args.kv_heads, args.q_heads, args.head_dim, args.batch, args.ctx
     bits = tagged_bits(B, N, seed_offset=rank * B)
+    if args.int2_frac is not None:
+        rng = np.random.default_rng(7 + rank)
+        bits = [np.where(rng.random(N) < args.int2_frac, 2, 4).astype(np.int8) for _ in range(B)]
     g = 32
     n_pages = [int((b == 2).sum()) // g for b in bits]
     n_int4 = [N - p * g for p in n_pages]

@@ -24,8 +24,14 @@
 
 namespace kvmix {
 
-constexpr int NW = 4;      // warps per CTA
-constexpr int STAGES = 3;  // ring depth per warp
+#ifndef KVMIX_STAGES
+#define KVMIX_STAGES 3
+#endif
+#ifndef KVMIX_MINB
+#define KVMIX_MINB 3
+#endif
+constexpr int NW = 4;                 // warps per CTA
+constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr uint32_t MAGIC = 0x3C003C00u;
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -38,8 +44,7 @@ struct Cfg {
   static constexpr int TB4 = tok_bytes(D, 4);
   static constexpr int PS = page_stride(D);
   static constexpr int SS = slot_stride(D);
-  static constexpr int SSM = D == 128 ? 176 : (D == 64 ? 80 : 48);  // smem slot stride, == 16 mod 32 (bank spread)
-  static constexpr int BUF = PS > 32 * SSM ? PS : 32 * SSM;
+  static constexpr int BUF = PS > 32 * SS ? PS : 32 * SS;  // one INT2 page or 32 INT4 slots (slot-contiguous)
   static constexpr int SMEM = NW * STAGES * BUF;
 };
 
@@ -217,19 +222,19 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
   using C = Cfg<D>;
   const int g = lane >> 2, q = lane & 3;
   // lane g reads byte beta(g) = (g>>1) | ((g&1)<<2) of every channel word -> tokens 4beta..4beta+3
+  // chunk i, lane q: k pair (2q, 2q+1) = channels 16i+4q+{0,1}, (2q+8, 2q+9) = 16i+4q+{2,3}
   const uint32_t selK = (uint32_t)(g >> 1) | ((uint32_t)(4 + (g >> 1)) << 8);
-  const uint8_t* kb = buf + 16 * q + 4 * (g & 1);  // + 128 i (+8 second channel, +64 / +72 channel+8)
-  const uint8_t* pb = buf + 8 * D + 8 * q;          // params of channel 16i+2q: + 64 i (+32 for +8)
+  const uint8_t* kb = buf + 32 * q + 4 * (g & 1);  // channel word 16i+4q+e: + 128 i + 8 e
+  const uint8_t* pb = buf + 8 * D + 16 * q;         // (s, z) of channels 16i+4q+{0..3}: + 64 i
   float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < C::NCH; ++i) {
     const uint32_t r1 = prmt(ld_s32(kb, 128 * i), ld_s32(kb, 128 * i + 8), selK);
-    const uint32_t r2 = prmt(ld_s32(kb, 128 * i + 64), ld_s32(kb, 128 * i + 72), selK);
-    const uint2 p1 = *reinterpret_cast<const uint2*>(pb + 64 * i);
-    const uint2 p2 = *reinterpret_cast<const uint2*>(pb + 64 * i + 32);
-    const uint64_t qs = pack_b64(hmul2u(lo32(qb2[i]), prmt(p1.x, p1.y, 0x5410)),
-                                 hmul2u(hi32(qb2[i]), prmt(p2.x, p2.y, 0x5410)));
-    const uint32_t z1 = prmt(p1.x, p1.y, 0x7632), z2 = prmt(p2.x, p2.y, 0x7632);
+    const uint32_t r2 = prmt(ld_s32(kb, 128 * i + 16), ld_s32(kb, 128 * i + 24), selK);
+    const uint4 pv = *reinterpret_cast<const uint4*>(pb + 64 * i);
+    const uint64_t qs = pack_b64(hmul2u(lo32(qb2[i]), prmt(pv.x, pv.y, 0x5410)),
+                                 hmul2u(hi32(qb2[i]), prmt(pv.z, pv.w, 0x5410)));
+    const uint32_t z1 = prmt(pv.x, pv.y, 0x7632), z2 = prmt(pv.z, pv.w, 0x7632);
     mma16816_b64(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qs);
     mma16816_b64(c1, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qs);
     // bias rows g carry sum_c q_c z_c; rows g+8 (cb[2], cb[3]) are don't-care filler
@@ -277,10 +282,13 @@ template <int D, bool FULL>
 __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const uint64_t (&qb4)[D / 16],
                                           int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
-  constexpr int S = C::SSM;
+  constexpr int S = C::SS;
   const int g = lane >> 2, q = lane & 3;
-  const uint8_t* kb = buf + S * g + 4 * q;  // slot row r: + S*(16(r>>1) + 8(r&1)); group j: + 16j
-  const uint8_t* kp = buf + S * g + D / 2;  // K params of the slot: + 4j
+  // QK row g of M tile m is slot 16m + beta(g), row g+8 is slot 16m + 8 + beta(g), with
+  // beta(g) = (g>>1) | ((g&1)<<2): PV lanes then read 4 slots 1 apart (conflict-free V loads)
+  const int beta = (g >> 1) | ((g & 1) << 2);
+  const uint8_t* kb = buf + S * beta + 4 * q;  // slot row r: + S*(16(r>>1) + 8(r&1)); group j: + 16j
+  const uint8_t* kp = buf + S * beta + D / 2;  // K params of the slot: + 4j
   float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int j = 0; j < C::NGRP; ++j) {
@@ -304,38 +312,39 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
   }
   float sv[8] = {c0[0], c0[1], c0[2], c0[3], c1[0], c1[1], c1[2], c1[3]};
   if (!FULL) {
-    if (g >= nv) sv[0] = sv[1] = -INFINITY;
-    if (g + 8 >= nv) sv[2] = sv[3] = -INFINITY;
-    if (g + 16 >= nv) sv[4] = sv[5] = -INFINITY;
-    if (g + 24 >= nv) sv[6] = sv[7] = -INFINITY;
+    if (beta >= nv) sv[0] = sv[1] = -INFINITY;
+    if (beta + 8 >= nv) sv[2] = sv[3] = -INFINITY;
+    if (beta + 16 >= nv) sv[4] = sv[5] = -INFINITY;
+    if (beta + 24 >= nv) sv[6] = sv[7] = -INFINITY;
   }
   uint32_t bP[2][2];
   softmax_tile<D>(sv, st, acc, bP);
   const uint32_t b4 = 2 * (g & 1);
   const uint32_t selV = b4 | ((b4 + 1) << 4) | ((b4 + 4) << 8) | ((b4 + 5) << 12);
-  const uint8_t* vb = buf + S * 2 * q + C::TB4;  // slot 2q's V block: + S*(16ks [+1] [+8])
-  const uint8_t* vc = vb + 4 * (g >> 1);         // + 16j: word holding bytes 16j+2g, +1
+  // PV k-step ks: pair A = QK rows (2q, 2q+1) = slots 16ks + q, 16ks + q + 4; pair B = + 8
+  const uint8_t* vb = buf + S * q + C::TB4;  // slot q's V block
+  const uint8_t* vc = vb + 4 * (g >> 1);     // + 16j: word holding bytes 16j+2g, +1
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
     uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
     lds_params<C::NGRP>(vb + S * (16 * ks) + D / 2, pA0);
-    lds_params<C::NGRP>(vb + S * (16 * ks + 1) + D / 2, pA1);
+    lds_params<C::NGRP>(vb + S * (16 * ks + 4) + D / 2, pA1);
     lds_params<C::NGRP>(vb + S * (16 * ks + 8) + D / 2, pB0);
-    lds_params<C::NGRP>(vb + S * (16 * ks + 9) + D / 2, pB1);
+    lds_params<C::NGRP>(vb + S * (16 * ks + 12) + D / 2, pB1);
     if (!FULL) {
-      const int sA0 = 16 * ks + 2 * q;
+      const int sA0 = 16 * ks + q;
 #pragma unroll
       for (int j = 0; j < C::NGRP; ++j) {
         if (sA0 >= nv) pA0[j] = 0u;
-        if (sA0 + 1 >= nv) pA1[j] = 0u;
+        if (sA0 + 4 >= nv) pA1[j] = 0u;
         if (sA0 + 8 >= nv) pB0[j] = 0u;
-        if (sA0 + 9 >= nv) pB1[j] = 0u;
+        if (sA0 + 12 >= nv) pB1[j] = 0u;
       }
     }
 #pragma unroll
     for (int j = 0; j < C::NGRP; ++j) {
-      const uint32_t rA = prmt(ld_s32(vc, S * (16 * ks) + 16 * j), ld_s32(vc, S * (16 * ks + 1) + 16 * j), selV);
-      const uint32_t rB = prmt(ld_s32(vc, S * (16 * ks + 8) + 16 * j), ld_s32(vc, S * (16 * ks + 9) + 16 * j), selV);
+      const uint32_t rA = prmt(ld_s32(vc, S * (16 * ks) + 16 * j), ld_s32(vc, S * (16 * ks + 4) + 16 * j), selV);
+      const uint32_t rB = prmt(ld_s32(vc, S * (16 * ks + 8) + 16 * j), ld_s32(vc, S * (16 * ks + 12) + 16 * j), selV);
       uint32_t fA[4], fB[4];
       fA[0] = hsub2u(lop_and_or(rA, 0x000F000Fu, MAGIC), MAGIC);
       fA[1] = hsub2u(lop_and_or(rA >> 2, 0x003C003Cu, MAGIC), MAGIC);
@@ -351,7 +360,7 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
 }
 
 template <int D>
-__global__ void __launch_bounds__(NW * 32, 3) decode_mma_kernel(const DecodeArgs a) {
+__global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[NW][STAGES];
@@ -378,7 +387,8 @@ __global__ void __launch_bounds__(NW * 32, 3) decode_mma_kernel(const DecodeArgs
 #pragma unroll
     for (int i = 0; i < C::NCH; ++i) {
       const int c1 = 16 * i + 2 * q;
-      qb2[i] = pack_b64(pack_h2(qv(c1), qv(c1 + 1)), pack_h2(qv(c1 + 8), qv(c1 + 9)));
+      const int c2 = 16 * i + 4 * q;
+      qb2[i] = pack_b64(pack_h2(qv(c2), qv(c2 + 1)), pack_h2(qv(c2 + 2), qv(c2 + 3)));
       const int base = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
       qb4[i] = pack_b64(pack_h2(qv(base + 0), qv(base + 4)), pack_h2(qv(base + 1), qv(base + 5)));
     }
@@ -401,13 +411,19 @@ __global__ void __launch_bounds__(NW * 32, 3) decode_mma_kernel(const DecodeArgs
         bulk_g2s(buf, kv2 + page * C::PS, C::PS, bar);
       }
     } else {
+      // one bulk copy per run of consecutive INT4 slots (fresh pools give long runs)
       const int it = t - u.npg;
       const int nv = min(32, u.n4 - 32 * it);
+      const int slot = lane < nv ? a.int4_ids[u.i40 + 32 * it + lane] : 0;
+      const int prev = __shfl_up_sync(0xffffffffu, slot, 1);
+      const bool start = lane < nv && (lane == 0 || slot != prev + 1);
+      const uint32_t starts = __ballot_sync(0xffffffffu, start);
       if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
       __syncwarp();
-      if (lane < nv) {
-        const int64_t slot = a.int4_ids[u.i40 + 32 * it + lane];
-        bulk_g2s(buf + lane * C::SSM, kv4 + slot * C::SS, C::SS, bar);
+      if (start) {
+        const uint32_t later = starts & ~((2u << lane) - 1u);
+        const int end = later ? __ffs(later) - 1 : nv;
+        bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)slot * C::SS, (end - lane) * C::SS, bar);
       }
     }
   };
