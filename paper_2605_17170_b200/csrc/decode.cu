@@ -34,6 +34,7 @@ constexpr int NW = 4;                 // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr uint32_t MAGIC = 0x3C003C00u;
 constexpr float LOG2E = 1.4426950408889634f;
+constexpr float RESCALE_SLACK = 8.f;  // see softmax_tile
 
 template <int D>
 struct Cfg {
@@ -150,9 +151,8 @@ struct Softmax {
 
 template <int D>
 struct Acc {
-  float o[D / 16][4];   // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
-  float zs[D / 32][4];  // sum_t p * z per channel group
-  uint32_t one[4];      // A operand of all-ones (fp16 1.0) kept in one register quad
+  float o[D / 16][4];  // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
+  float zs[4];         // Z^T.P^T: row j (< D/32) = sum_t z_tj p_th (rows >= D/32 unused)
 };
 
 __device__ __forceinline__ uint32_t ld_s32(const uint8_t* base, int off) {
@@ -169,8 +169,11 @@ __device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, 
     tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
     tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
   }
-  const float mn0 = fmaxf(st.m0, tm0), mn1 = fmaxf(st.m1, tm1);
-  if (__any_sync(0xffffffffu, (mn0 != st.m0) || (mn1 != st.m1))) {
+  // Lazy rescale: keep the stale running max until a tile exceeds it by > RESCALE_SLACK
+  // (log2 units); p then stays <= 2^RESCALE_SLACK, well inside fp16, and the exact
+  // rescale happens only when needed (rarely after the first tiles).
+  if (__any_sync(0xffffffffu, (tm0 > st.m0 + RESCALE_SLACK) || (tm1 > st.m1 + RESCALE_SLACK))) {
+    const float mn0 = fmaxf(st.m0, tm0), mn1 = fmaxf(st.m1, tm1);
     const float al0 = fast_exp2(st.m0 - mn0), al1 = fast_exp2(st.m1 - mn1);  // exp2(-inf) = 0
     st.l0 *= al0;
     st.l1 *= al1;
@@ -179,14 +182,12 @@ __device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, 
       acc.o[m][0] *= al0; acc.o[m][2] *= al0;
       acc.o[m][1] *= al1; acc.o[m][3] *= al1;
     }
-#pragma unroll
-    for (int j = 0; j < D / 32; ++j) {
-      acc.zs[j][0] *= al0; acc.zs[j][2] *= al0;
-      acc.zs[j][1] *= al1; acc.zs[j][3] *= al1;
-    }
+    acc.zs[0] *= al0; acc.zs[2] *= al0;
+    acc.zs[1] *= al1; acc.zs[3] *= al1;
     st.m0 = mn0;
     st.m1 = mn1;
   }
+  const float mn0 = st.m0, mn1 = st.m1;
   float p[8];
 #pragma unroll
   for (int i = 0; i < 8; i += 2) {
@@ -203,16 +204,24 @@ __device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, 
 }
 
 // PV for one k-step and one channel group j: A = code fields of the pair-A / pair-B
-// tokens (rows e = 0..3 -> channels 32j + 4g + e), B = P' = p*s and P*z.
+// tokens (rows e = 0..3 -> channels 32j + 4g + e), B = P' = p*s.
 template <int D>
 __device__ __forceinline__ void pv_group(Acc<D>& acc, int j, const uint32_t (&fA)[4], const uint32_t (&fB)[4],
                                          uint32_t bP0, uint32_t bP1, uint32_t pA0, uint32_t pA1, uint32_t pB0,
                                          uint32_t pB1) {
   const uint64_t ps = pack_b64(hmul2u(bP0, prmt(pA0, pA1, 0x5410)), hmul2u(bP1, prmt(pB0, pB1, 0x5410)));
-  const uint64_t pz = pack_b64(hmul2u(bP0, prmt(pA0, pA1, 0x7632)), hmul2u(bP1, prmt(pB0, pB1, 0x7632)));
   mma16816_b64(acc.o[2 * j], fA[0], fA[1], fB[0], fB[1], ps);
   mma16816_b64(acc.o[2 * j + 1], fA[2], fA[3], fB[2], fB[3], ps);
-  mma16816_b64(acc.zs[j], acc.one[0], acc.one[1], acc.one[2], acc.one[3], pz);  // sum_t p*z
+}
+
+// sum_t p_th z_tj for all groups j at once: A = Z^T (row g = group g&3, k = PV tokens),
+// B = P^T.  zA0..zB1 are the (scale, zero) words of group g&3 of the 4 tokens.
+template <int D>
+__device__ __forceinline__ void pv_zeros(Acc<D>& acc, uint32_t zA0, uint32_t zA1, uint32_t zB0, uint32_t zB1,
+                                         uint32_t bP0, uint32_t bP1) {
+  const uint32_t zA = prmt(zA0, zA1, 0x7632), zB = prmt(zB0, zB1, 0x7632);
+  // rows g+8 (a1, a3) are don't-care: feed the raw words to avoid register moves
+  mma16816_b64(acc.zs, zA, zA0, zB, zB0, pack_b64(bP0, bP1));
 }
 
 // ---------------------------------- INT2 page tile ----------------------------------
@@ -258,6 +267,11 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
     lds_params<C::NGRP>(vb + (16 + 2 * ks) * T + D / 4, pA1);
     lds_params<C::NGRP>(vb + (2 * ks + 1) * T + D / 4, pB0);
     lds_params<C::NGRP>(vb + (17 + 2 * ks) * T + D / 4, pB1);
+    {
+      const uint8_t* zb = vb + D / 4 + 4 * (g & (C::NGRP - 1));
+      pv_zeros<D>(acc, ld_s32(zb, (2 * ks) * T), ld_s32(zb, (16 + 2 * ks) * T), ld_s32(zb, (2 * ks + 1) * T),
+                  ld_s32(zb, (17 + 2 * ks) * T), bP[ks][0], bP[ks][1]);
+    }
 #pragma unroll
     for (int j = 0; j < C::NGRP; ++j) {
       const uint32_t rA = prmt(ld_s32(vc, (2 * ks) * T + 8 * j), ld_s32(vc, (16 + 2 * ks) * T + 8 * j), selV);
@@ -341,6 +355,19 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
         if (sA0 + 12 >= nv) pB1[j] = 0u;
       }
     }
+    {
+      const uint8_t* zb = vb + D / 2 + 4 * (g & (C::NGRP - 1));
+      uint32_t zA0 = ld_s32(zb, S * (16 * ks)), zA1 = ld_s32(zb, S * (16 * ks + 4));
+      uint32_t zB0 = ld_s32(zb, S * (16 * ks + 8)), zB1 = ld_s32(zb, S * (16 * ks + 12));
+      if (!FULL) {
+        const int sA0 = 16 * ks + q;
+        if (sA0 >= nv) zA0 = 0u;
+        if (sA0 + 4 >= nv) zA1 = 0u;
+        if (sA0 + 8 >= nv) zB0 = 0u;
+        if (sA0 + 12 >= nv) zB1 = 0u;
+      }
+      pv_zeros<D>(acc, zA0, zA1, zB0, zB1, bP[ks][0], bP[ks][1]);
+    }
 #pragma unroll
     for (int j = 0; j < C::NGRP; ++j) {
       const uint32_t rA = prmt(ld_s32(vc, S * (16 * ks) + 16 * j), ld_s32(vc, S * (16 * ks + 4) + 16 * j), selV);
@@ -376,8 +403,52 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   }
   __syncwarp();
 
+  const int ntiles = u.thi - u.tlo;
+  const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
+  const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
+  const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
+
+  // tile metadata: the page id (INT2 tile) or this lane's slot (INT4 tile); loaded one
+  // iteration before its copy is issued so the copy never waits on the index load
+  auto load_meta = [&](int k) -> int {
+    if (k >= nmine) return 0;
+    const int t = u.tlo + warp + k * NW;
+    if (t < u.npg) return a.page_ids[u.pg0 + t];
+    const int it = t - u.npg;
+    return lane < min(32, u.n4 - 32 * it) ? a.int4_ids[u.i40 + 32 * it + lane] : 0;
+  };
+  auto issue = [&](int k, int meta, int s) {
+    const int t = u.tlo + warp + k * NW;
+    uint8_t* buf = ring + s * C::BUF;
+    uint64_t* bar = &bars[warp][s];
+    if (t < u.npg) {
+      if (lane == 0) {
+        mbar_expect_tx(bar, C::PS);
+        bulk_g2s(buf, kv2 + (int64_t)meta * C::PS, C::PS, bar);
+      }
+    } else {
+      // one bulk copy per run of consecutive INT4 slots (fresh pools give long runs)
+      const int nv = min(32, u.n4 - 32 * (t - u.npg));
+      const int prev = __shfl_up_sync(0xffffffffu, meta, 1);
+      const bool start = lane < nv && (lane == 0 || meta != prev + 1);
+      const uint32_t starts = __ballot_sync(0xffffffffu, start);
+      if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
+      __syncwarp();
+      if (start) {
+        const uint32_t later = starts & ~((2u << lane) - 1u);
+        const int end = later ? __ffs(later) - 1 : nv;
+        bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)meta * C::SS, (end - lane) * C::SS, bar);
+      }
+    }
+  };
+  {
+    int s0 = 0;
+    for (int k = 0; k < STAGES && k < nmine; ++k) issue(k, load_meta(k), s0++);
+  }
+  int meta_next = load_meta(STAGES);
+
   // ---- Q fragments (B operand of QK), fp16, pre-scaled by scale*log2(e) ----
-  // qb2: INT2 key pages, chunk i covers channels 16i..16i+15 in natural order.
+  // qb2: INT2 key pages, chunk i, lane q: pairs (16i+4q+{0,1}) and (16i+4q+{2,3}).
   // qb4: INT4 keys, chunk 2j+s pairs channels (32j+8q+{0,4}/{1,5}) (s=0) or ({2,6}/{3,7}) (s=1).
   uint64_t qb2[C::NCH], qb4[C::NCH];
   {
@@ -386,7 +457,6 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     auto qv = [&](int c) { return hv ? load_q(a, qrow + c) * a.qscale : 0.f; };
 #pragma unroll
     for (int i = 0; i < C::NCH; ++i) {
-      const int c1 = 16 * i + 2 * q;
       const int c2 = 16 * i + 4 * q;
       qb2[i] = pack_b64(pack_h2(qv(c2), qv(c2 + 1)), pack_h2(qv(c2 + 2), qv(c2 + 3)));
       const int base = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
@@ -394,55 +464,21 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     }
   }
 
-  const int ntiles = u.thi - u.tlo;
-  const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
-  const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
-  const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
-
-  auto issue = [&](int k) {
-    const int t = u.tlo + warp + k * NW;
-    const int s = k % STAGES;
-    uint8_t* buf = ring + s * C::BUF;
-    uint64_t* bar = &bars[warp][s];
-    if (t < u.npg) {
-      if (lane == 0) {
-        const int64_t page = a.page_ids[u.pg0 + t];
-        mbar_expect_tx(bar, C::PS);
-        bulk_g2s(buf, kv2 + page * C::PS, C::PS, bar);
-      }
-    } else {
-      // one bulk copy per run of consecutive INT4 slots (fresh pools give long runs)
-      const int it = t - u.npg;
-      const int nv = min(32, u.n4 - 32 * it);
-      const int slot = lane < nv ? a.int4_ids[u.i40 + 32 * it + lane] : 0;
-      const int prev = __shfl_up_sync(0xffffffffu, slot, 1);
-      const bool start = lane < nv && (lane == 0 || slot != prev + 1);
-      const uint32_t starts = __ballot_sync(0xffffffffu, start);
-      if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
-      __syncwarp();
-      if (start) {
-        const uint32_t later = starts & ~((2u << lane) - 1u);
-        const int end = later ? __ffs(later) - 1 : nv;
-        bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)slot * C::SS, (end - lane) * C::SS, bar);
-      }
-    }
-  };
-  for (int k = 0; k < STAGES && k < nmine; ++k) issue(k);
 
   Acc<D> acc;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) asm volatile("mov.b32 %0, 0x3c003c00;" : "=r"(acc.one[i]));
-#pragma unroll
   for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
-#pragma unroll
-  for (int j = 0; j < C::NGRP; ++j) acc.zs[j][0] = acc.zs[j][1] = acc.zs[j][2] = acc.zs[j][3] = 0.f;
+  acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
   Softmax st{-INFINITY, -INFINITY, 0.f, 0.f};
 
+  int stage = 0;
+  uint32_t phase = 0;
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
-    const int s = k % STAGES;
-    const uint8_t* buf = ring + s * C::BUF;
-    mbar_wait(&bars[warp][s], (uint32_t)((k / STAGES) & 1));
+    const uint8_t* buf = ring + stage * C::BUF;
+    const int meta = meta_next;
+    meta_next = load_meta(k + STAGES + 1);
+    mbar_wait(&bars[warp][stage], phase);
     if (t < u.npg) {
       int2_tile<D>(buf, qb2, lane, st, acc);
     } else {
@@ -453,7 +489,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     __syncwarp();
     if (k + STAGES < nmine) {
       fence_proxy_async();
-      issue(k + STAGES);
+      issue(k + STAGES, meta, stage);
+    }
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1u;
     }
   }
 
@@ -467,16 +507,22 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   float* sm_acc = reinterpret_cast<float*>(smem);
   float* sm_m = sm_acc + NW * 8 * D;
   float* sm_l = sm_m + NW * 8;
+  float z0[C::NGRP], z1[C::NGRP];  // sum_t p z of group j for heads 2q, 2q+1 (from lane (j, q))
+#pragma unroll
+  for (int j = 0; j < C::NGRP; ++j) {
+    z0[j] = __shfl_sync(0xffffffffu, acc.zs[0], 4 * j + q);
+    z1[j] = __shfl_sync(0xffffffffu, acc.zs[1], 4 * j + q);
+  }
 #pragma unroll
   for (int m = 0; m < C::NCH; ++m) {
     const int j = m >> 1;
     const int e0 = 2 * (m & 1);
     const int ch0 = 32 * j + 4 * g + e0;
     const float f0 = (float)(1 << (10 - 2 * e0)), f1 = (float)(1 << (10 - 2 * (e0 + 1)));
-    sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, acc.zs[j][0]);
-    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, acc.zs[j][1]);
-    sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, acc.zs[j][0]);
-    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(acc.o[m][3], f1, acc.zs[j][1]);
+    sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, z0[j]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, z1[j]);
+    sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, z0[j]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(acc.o[m][3], f1, z1[j]);
   }
   if (g == 0) {
     sm_m[warp * 8 + 2 * q] = st.m0;
