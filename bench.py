@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--head-dim", type=int, default=128)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--int2-frac", type=float, default=None, help="override: i.i.d. bits with this INT2 fraction")
+    ap.add_argument("--plan-waves", type=float, default=2.0, help="split planner: target waves of CTAs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-units", type=int, default=0, help="(request, layer) units timed on CPU")
@@ -251,7 +252,7 @@ def build_workload(args, device, rank: int):
         pool.partition(table)
         rids.append(rid)
     torch.cuda.synchronize()
-    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq)
+    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq, waves=args.plan_waves, ctas_per_sm=3)
     q = torch.randn((L, B, Hq, d), device=device, generator=gen).to(torch.bfloat16)
     out = torch.empty_like(q)
     return pool, batch, q, out, bits

@@ -111,7 +111,8 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
  *     bitwidth-homogeneous per tile, never straddling pages)
  *   part_indptr[batch*Hkv + 1]: partial slots of each unit (contiguous)
  *   workspace: >= n_parts * (n_q_heads/Hkv) * (d + 2) floats
- *   variant: 0 = tensor-core kernel (mma.sync m16n8k16), 1 = simple CUDA-core kernel;
+ *   variant: 0 = tensor-core kernel (mma.sync m16n8k16), 1 = simple CUDA-core kernel,
+ *     2 = data movement only, 3 = compute only on stale smem (measurement; output meaningless);
  *     | 0x100 = write the partials only (skip K3; used to time K2 alone)
  * Requires n_q_heads % Hkv == 0 and n_q_heads / Hkv <= 8, d in {32, 64, 128}. */
 int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype, const uint8_t* int2_pool,

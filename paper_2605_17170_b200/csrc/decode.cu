@@ -241,13 +241,13 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
     const uint32_t r1 = prmt(ld_s32(kb, 128 * i), ld_s32(kb, 128 * i + 8), selK);
     const uint32_t r2 = prmt(ld_s32(kb, 128 * i + 16), ld_s32(kb, 128 * i + 24), selK);
     const uint4 pv = *reinterpret_cast<const uint4*>(pb + 64 * i);
-    const uint64_t qs = pack_b64(hmul2u(lo32(qb2[i]), prmt(pv.x, pv.y, 0x5410)),
-                                 hmul2u(hi32(qb2[i]), prmt(pv.z, pv.w, 0x5410)));
+    const uint64_t qi = qb2[i];
+    const uint64_t qs = pack_b64(hmul2u(lo32(qi), prmt(pv.x, pv.y, 0x5410)), hmul2u(hi32(qi), prmt(pv.z, pv.w, 0x5410)));
     const uint32_t z1 = prmt(pv.x, pv.y, 0x7632), z2 = prmt(pv.z, pv.w, 0x7632);
     mma16816_b64(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qs);
     mma16816_b64(c1, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qs);
     // bias rows g carry sum_c q_c z_c; rows g+8 (cb[2], cb[3]) are don't-care filler
-    mma16816_b64(cb, z1, r1, z2, r2, qb2[i]);
+    mma16816_b64(cb, z1, r1, z2, r2, qi);
   }
   // undo 2^(2k-10) per token row (k = token position inside its code byte)
   const float sv[8] = {fmaf(c0[0], 1024.f, cb[0]), fmaf(c0[1], 1024.f, cb[1]), fmaf(c0[2], 256.f, cb[0]),
@@ -319,10 +319,11 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
       e[r][2] = int4_deq(lop_and_or(w >> 2, 0x03C003C0u, MAGIC), s16, zz);
       e[r][3] = int4_deq(lop_and_or(w >> 6, 0x03C003C0u, MAGIC), s16, zz);
     }
-    mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], qb4[2 * j]);
-    mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], qb4[2 * j + 1]);
-    mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], qb4[2 * j]);
-    mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], qb4[2 * j + 1]);
+    const uint64_t qa = qb4[2 * j], qc = qb4[2 * j + 1];
+    mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], qa);
+    mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], qc);
+    mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], qa);
+    mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], qc);
   }
   float sv[8] = {c0[0], c0[1], c0[2], c0[3], c1[0], c1[1], c1[2], c1[3]};
   if (!FULL) {
@@ -386,7 +387,7 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
   }
 }
 
-template <int D>
+template <int D, bool COMPUTE = true, bool MEMORY = true>
 __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       }
     }
   };
-  {
+  if (MEMORY) {
     int s0 = 0;
     for (int k = 0; k < STAGES && k < nmine; ++k) issue(k, load_meta(k), s0++);
   }
@@ -464,7 +465,6 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     }
   }
 
-
   Acc<D> acc;
 #pragma unroll
   for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
@@ -478,8 +478,10 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     const uint8_t* buf = ring + stage * C::BUF;
     const int meta = meta_next;
     meta_next = load_meta(k + STAGES + 1);
-    mbar_wait(&bars[warp][stage], phase);
-    if (t < u.npg) {
+    if (MEMORY) mbar_wait(&bars[warp][stage], phase);
+    if (!COMPUTE) {
+      // measurement variant: data movement only (no dequant / MMA)
+    } else if (t < u.npg) {
       int2_tile<D>(buf, qb2, lane, st, acc);
     } else {
       const int nv = min(32, u.n4 - 32 * (t - u.npg));
@@ -487,7 +489,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       else int4_tile<D, false>(buf, nv, qb4, lane, st, acc);
     }
     __syncwarp();
-    if (k + STAGES < nmine) {
+    if (MEMORY && k + STAGES < nmine) {
       fence_proxy_async();
       issue(k + STAGES, meta, stage);
     }
@@ -656,6 +658,21 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, bool 
       attr_set = true;
     }
     decode_mma_kernel<D><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
+  } else if (variant == 3) {
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaFuncSetAttribute(decode_mma_kernel<D, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Cfg<D>::SMEM);
+      attr3 = true;
+    }
+    decode_mma_kernel<D, true, false><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
+  } else if (variant == 2) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(decode_mma_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
+      attr2 = true;
+    }
+    decode_mma_kernel<D, false><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
   } else {
     decode_simple_kernel<D><<<(unsigned)n_work, NW * 32, 0, s>>>(a);
   }
@@ -704,7 +721,7 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
   const bool partials_only = (variant & 0x100) != 0;  // measurement hook: skip K3
   variant &= 0xff;
-  if (variant != 0 && variant != 1) return fail(KVMIX_EINVAL, "bad variant");
+  if (variant < 0 || variant > 3) return fail(KVMIX_EINVAL, "bad variant");
   (void)workspace_floats;
   DecodeArgs a;
   a.q = q;
