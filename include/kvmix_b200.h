@@ -102,25 +102,25 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
 /* ---- decode attention (K2 + K3) ---------------------------------------------------- */
 
 /* Replaces attention.py:175 flash_decode (+ PoolView.gather pool.py:394, _split_partial
- * attention.py:168, merge_partials attention.py:154), batched over requests, one layer.
+ * attention.py:168, merge_partials attention.py:154), batched over requests, one layer,
+ * one launch (the cross-split combine is fused into the kernel).
  *   q [batch][n_q_heads][d] (q_dtype), out [batch][n_q_heads][d] (out_dtype)
  *   page_indptr[batch+1], page_ids[]: INT2 page list of each partitioned table (table order)
  *   int4_indptr[batch+1], int4_ids[]: INT4 indices of each table's suffix (table order)
- *   work [n_work][4] = {unit = b*Hkv + kvh, tile_lo, tile_hi, partial_slot}; the tiles of a
- *     unit are its INT2 pages then ceil(n_int4/32) INT4 tiles of 32 slots (splits are
- *     bitwidth-homogeneous per tile, never straddling pages)
- *   part_indptr[batch*Hkv + 1]: partial slots of each unit (contiguous)
- *   workspace: >= n_parts * (n_q_heads/Hkv) * (d + 2) floats
+ *   work [n_work][4] = {unit = b*Hkv + kvh, tile_lo, tile_hi, reserved}, unit-major with the
+ *     same number S = n_work / (batch*Hkv) in 1..8 of splits per unit; the tiles of a unit
+ *     are its INT2 pages then ceil(n_int4/32) INT4 tiles of 32 slots (every tile is
+ *     bitwidth-homogeneous).  The S CTAs of a unit run as one thread-block cluster and
+ *     merge their (m, l, acc) through distributed shared memory.
  *   variant: 0 = tensor-core kernel (mma.sync m16n8k16), 1 = simple CUDA-core kernel,
- *     2 = data movement only, 3 = compute only on stale smem (measurement; output meaningless);
- *     | 0x100 = write the partials only (skip K3; used to time K2 alone)
+ *     2 = data movement only, 3 = compute only on stale smem (measurement; output meaningless)
  * Requires n_q_heads % Hkv == 0 and n_q_heads / Hkv <= 8, d in {32, 64, 128}. */
 int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype, const uint8_t* int2_pool,
                        const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
                        int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
                        const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
-                       const int32_t* int4_ids, const int32_t* work, int64_t n_work, const int32_t* part_indptr,
-                       float* workspace, int64_t workspace_floats, float scale, int32_t variant, void* stream);
+                       const int32_t* int4_ids, const int32_t* work, int64_t n_work, float scale, int32_t variant,
+                       void* stream);
 
 /* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
  * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */

@@ -4,7 +4,8 @@ Drop-in for the decode half of /root/reference/pkg/src/kvmix/attention.py:
 ``flash_decode`` keeps its signature (:175) and validation order (:188-201) and
 returns a numpy [H, d] float32 array like the reference; ``merge_partials`` (:154)
 and ``SplitPartial`` (:145) keep their meaning.  The work is done by the sm_100a
-kernels K2 (tensor-core split decode) + K3 (combine) of libkvmix_b200.
+kernel K2 of libkvmix_b200 (tensor-core split decode whose last CTA per
+(request, kv head) merges the split partials -- the combine K3 is fused in).
 
 ``DecodeBatch`` / ``flash_decode_batched`` are the native hot-path API: a batch of
 requests, one layer per call, q/out as device tensors, page tables resident on the
@@ -54,7 +55,7 @@ def merge_partials(parts: Sequence[SplitPartial]) -> np.ndarray:
 
 
 class DecodeBatch:
-    """Device-resident CSR page tables + split plan + workspace for a request batch."""
+    """Device-resident CSR page tables + split plan for a request batch."""
 
     def __init__(self, pool: MixedPrecisionPool, request_ids=None, n_q_heads: int | None = None,
                  tables: list | None = None, **plan_kw):
@@ -81,15 +82,12 @@ class DecodeBatch:
             t = pool.device_tables(self.request_ids)
         self.batch = int(t["n_pages"].size)
         self.csr = t
-        work, part_indptr, n_parts = plan_splits(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride,
-                                                 pool.slot_stride, **self.plan_kw)
+        work, splits = plan_splits(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride, pool.slot_stride,
+                                   **self.plan_kw)
         dev = pool.device
         self.work = torch.as_tensor(work, device=dev)
-        self.part_indptr = torch.as_tensor(part_indptr, device=dev)
         self.n_work = int(work.shape[0])
-        self.n_parts = int(n_parts)
-        gq = self.n_q_heads // cfg.n_kv_heads
-        self.workspace = torch.empty(max(1, n_parts * gq * (cfg.head_dim + 2)), dtype=torch.float32, device=dev)
+        self.splits = int(splits)
         self.n_tokens = t["n_pages"] * cfg.page_size + t["n_int4"]
 
     def kv_bytes(self) -> int:
@@ -124,8 +122,7 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
         q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
         pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,
         batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
-        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.n_work,
-        batch.part_indptr.data_ptr(), batch.workspace.data_ptr(), batch.workspace.numel(), float(scale),
+        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.n_work, float(scale),
         int(variant), _lib.stream()))
     return out
 

@@ -19,6 +19,8 @@
 //    group scale folds into P' = p*s, and sum_t p*z comes from an MMA with A = 1;
 //  * codes become fp16 with one LOP3 against the 0x3C00 exponent (1 + code*2^(p-10))
 //    and an exact HSUB2, leaving code * 2^(p-10); the power of two is undone per row.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -63,8 +65,7 @@ struct DecodeArgs {
   const int32_t* int4_indptr;
   const int32_t* int4_ids;
   const int32_t* work;
-  const int32_t* part_indptr;
-  float* ws;
+  int cluster;  // CTAs (splits) per (request, kv head) unit == thread-block cluster size
   float qscale;  // softmax scale * log2(e)
 };
 
@@ -96,7 +97,7 @@ __device__ __forceinline__ uint32_t int2_field(uint32_t r, int e) {
 // ------------------------------------------------------------------------------------
 // Work-item prologue shared by both kernel variants.
 struct Unit {
-  int b, kvh, tlo, thi, part, npg, n4;
+  int b, kvh, tlo, thi, npg, n4;
   int64_t pg0, i40;
 };
 __device__ __forceinline__ Unit load_unit(const DecodeArgs& a) {
@@ -107,7 +108,6 @@ __device__ __forceinline__ Unit load_unit(const DecodeArgs& a) {
   u.kvh = unit % a.n_kv;
   u.tlo = wk[1];
   u.thi = wk[2];
-  u.part = wk[3];
   u.pg0 = a.page_indptr[u.b];
   u.npg = a.page_indptr[u.b + 1] - (int)u.pg0;
   u.i40 = a.int4_indptr[u.b];
@@ -115,10 +115,22 @@ __device__ __forceinline__ Unit load_unit(const DecodeArgs& a) {
   return u;
 }
 
-// Merge the NW warps' (m, l, acc) per head through smem and write the work item's partial.
+__device__ __forceinline__ void store_out(const DecodeArgs& a, int64_t oi, float v) {
+  if (a.out_dtype == KVMIX_F32) reinterpret_cast<float*>(a.out)[oi] = v;
+  else if (a.out_dtype == KVMIX_BF16) reinterpret_cast<__nv_bfloat16*>(a.out)[oi] = __float2bfloat16(v);
+  else reinterpret_cast<__half*>(a.out)[oi] = __float2half(v);
+}
+
+// Epilogue shared by both variants (this is K3, the cross-split combine, fused in):
+// 1. merge the NW warps' (m, l, acc) per head through smem into this CTA's state;
+// 2. the `cluster` CTAs that split one (request, kv head) unit form a thread-block
+//    cluster: after a cluster barrier, CTA rank r merges a slice of the unit's outputs
+//    by reading every CTA's state through distributed shared memory (attention.py:154-165).
+// No global partials, no atomics, no second launch.
 template <int D>
-__device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit& u, float* sm_m, float* sm_l,
-                                                float* sm_acc) {
+__device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit& u, const float* sm_m,
+                                                const float* sm_l, const float* sm_acc, float* cm, float* cl,
+                                                float* cacc) {
   __syncthreads();
   for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
     const int hh = i / D, c = i % D;
@@ -133,13 +145,35 @@ __device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit&
       acc += f * sm_acc[(w * 8 + hh) * D + c];
       l += f * sm_l[w * 8 + hh];
     }
-    float* dst = a.ws + ((int64_t)u.part * a.gq + hh) * (D + 2);
-    dst[c] = acc;
-    if (c == 0) {
-      dst[D] = M;
-      dst[D + 1] = l;
+    if (a.cluster == 1) {
+      store_out(a, ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + hh) * D + c, acc / l);
+    } else {
+      cacc[hh * D + c] = acc;
+      if (c == 0) {
+        cm[hh] = M;
+        cl[hh] = l;
+      }
     }
   }
+  if (a.cluster == 1) return;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();  // every CTA of the unit has published its state in smem
+  const int ns = a.cluster, r = (int)cluster.block_rank();
+  for (int i = r * blockDim.x + threadIdx.x; i < a.gq * D; i += ns * blockDim.x) {
+    const int hh = i / D, c = i % D;
+    float M = -INFINITY;
+    for (int k = 0; k < ns; ++k) M = fmaxf(M, cluster.map_shared_rank(cm, k)[hh]);
+    float acc = 0.f, l = 0.f;
+    for (int k = 0; k < ns; ++k) {
+      const float mk = cluster.map_shared_rank(cm, k)[hh];
+      const float f = mk == -INFINITY ? 0.f : fast_exp2(mk - M);
+      acc = fmaf(cluster.map_shared_rank(cacc, k)[hh * D + c], f, acc);
+      l = fmaf(cluster.map_shared_rank(cl, k)[hh], f, l);
+    }
+    store_out(a, ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + hh) * D + c, acc / l);
+  }
+  cluster.sync();  // keep this CTA's smem alive until all ranks have read it
 }
 
 // ====================================================================================
@@ -509,6 +543,9 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   float* sm_acc = reinterpret_cast<float*>(smem);
   float* sm_m = sm_acc + NW * 8 * D;
   float* sm_l = sm_m + NW * 8;
+  float* cta_acc = sm_l + NW * 8;  // this CTA's merged state, read by the cluster
+  float* cta_m = cta_acc + 8 * D;
+  float* cta_l = cta_m + 8;
   float z0[C::NGRP], z1[C::NGRP];  // sum_t p z of group j for heads 2q, 2q+1 (from lane (j, q))
 #pragma unroll
   for (int j = 0; j < C::NGRP; ++j) {
@@ -532,7 +569,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     sm_l[warp * 8 + 2 * q] = st.l0;
     sm_l[warp * 8 + 2 * q + 1] = st.l1;
   }
-  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc);
+  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc, cta_m, cta_l, cta_acc);
 }
 
 // ====================================================================================
@@ -544,6 +581,7 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
   __shared__ float qs[8][D];
   __shared__ float sm_acc[NW * 8 * D];
   __shared__ float sm_m[NW * 8], sm_l[NW * 8];
+  __shared__ float cta_acc[8 * D], cta_m[8], cta_l[8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const Unit u = load_unit(a);
   for (int i = threadIdx.x; i < 8 * D; i += blockDim.x) {
@@ -617,69 +655,40 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
       sm_l[warp * 8 + h] = l[h];
     }
   }
-  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc);
+  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc, cta_m, cta_l, cta_acc);
 }
 
-// ====================================================================================
-// K3: merge the partials of each (request, q head) -> out.  attention.py:154-165.
-template <int D>
-__global__ void combine_kernel(const DecodeArgs a) {
-  const int bh = blockIdx.x;
-  const int b = bh / a.n_q, hq = bh % a.n_q;
-  const int kvh = hq / a.gq, hh = hq % a.gq;
-  const int unit = b * a.n_kv + kvh;
-  const int p0 = a.part_indptr[unit], p1 = a.part_indptr[unit + 1];
-  float M = -INFINITY;
-  for (int p = p0; p < p1; ++p) M = fmaxf(M, a.ws[((int64_t)p * a.gq + hh) * (D + 2) + D]);
-  for (int c = threadIdx.x; c < D; c += blockDim.x) {
-    float acc = 0.f, l = 0.f;
-    for (int p = p0; p < p1; ++p) {
-      const float* src = a.ws + ((int64_t)p * a.gq + hh) * (D + 2);
-      const float f = src[D] == -INFINITY ? 0.f : exp2f(src[D] - M);
-      acc = fmaf(src[c], f, acc);
-      l = fmaf(src[D + 1], f, l);
-    }
-    const float v = acc / l;
-    const int64_t oi = ((int64_t)b * a.n_q + hq) * D + c;
-    if (a.out_dtype == KVMIX_F32) reinterpret_cast<float*>(a.out)[oi] = v;
-    else if (a.out_dtype == KVMIX_BF16) reinterpret_cast<__nv_bfloat16*>(a.out)[oi] = __float2bfloat16(v);
-    else reinterpret_cast<__half*>(a.out)[oi] = __float2half(v);
+template <typename Kern>
+static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_work, int smem, cudaStream_t s) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
   }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n_work);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
+  return check_launch("flash_decode");
 }
 
 template <int D>
-static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, bool partials_only, cudaStream_t s) {
-  if (variant == 0) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           Cfg<D>::SMEM);
-      if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
-      attr_set = true;
-    }
-    decode_mma_kernel<D><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
-  } else if (variant == 3) {
-    static bool attr3 = false;
-    if (!attr3) {
-      cudaFuncSetAttribute(decode_mma_kernel<D, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           Cfg<D>::SMEM);
-      attr3 = true;
-    }
-    decode_mma_kernel<D, true, false><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
-  } else if (variant == 2) {
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(decode_mma_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
-      attr2 = true;
-    }
-    decode_mma_kernel<D, false><<<(unsigned)n_work, NW * 32, Cfg<D>::SMEM, s>>>(a);
-  } else {
-    decode_simple_kernel<D><<<(unsigned)n_work, NW * 32, 0, s>>>(a);
+static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaStream_t s) {
+  switch (variant) {
+    case 0: return launch_kernel(decode_mma_kernel<D, true, true>, a, n_work, Cfg<D>::SMEM, s);
+    case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, 0, s);
+    case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
+    default: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
   }
-  int rc = check_launch("flash_decode");
-  if (rc || partials_only) return rc;
-  combine_kernel<D><<<(unsigned)(a.batch * a.n_q), D, 0, s>>>(a);
-  return check_launch("flash_decode_combine");
 }
 
 // merge_partials (attention.py:154-165) for host-supplied partials, natural-log domain.
@@ -712,17 +721,16 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
                                   int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
                                   int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
                                   const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
-                                  int64_t n_work, const int32_t* part_indptr, float* workspace,
-                                  int64_t workspace_floats, float scale, int32_t variant, void* stream) {
+                                  int64_t n_work, float scale, int32_t variant, void* stream) {
   if (n_kv <= 0 || n_q % n_kv) return fail(KVMIX_EINVAL, "n_heads not a multiple of the pool's n_kv_heads");
   const int64_t gq = n_q / n_kv;
   if (gq > 8) return fail(KVMIX_EINVAL, "GQA group > 8 not supported");
   if (batch <= 0 || n_work <= 0) return fail(KVMIX_EINVAL, "empty batch or work list");
+  const int64_t units = batch * n_kv;
+  if (n_work % units || n_work / units > 8)
+    return fail(KVMIX_EINVAL, "work list must hold 1..8 splits per (request, kv head), unit-major");
   if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
-  const bool partials_only = (variant & 0x100) != 0;  // measurement hook: skip K3
-  variant &= 0xff;
   if (variant < 0 || variant > 3) return fail(KVMIX_EINVAL, "bad variant");
-  (void)workspace_floats;
   DecodeArgs a;
   a.q = q;
   a.q_dtype = q_dtype;
@@ -742,14 +750,13 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   a.int4_indptr = int4_indptr;
   a.int4_ids = int4_ids;
   a.work = work;
-  a.part_indptr = part_indptr;
-  a.ws = workspace;
+  a.cluster = (int)(n_work / units);
   a.qscale = scale * LOG2E;
   cudaStream_t s = (cudaStream_t)stream;
   switch (d) {
-    case 32: return launch_decode<32>(a, n_work, variant, partials_only, s);
-    case 64: return launch_decode<64>(a, n_work, variant, partials_only, s);
-    case 128: return launch_decode<128>(a, n_work, variant, partials_only, s);
+    case 32: return launch_decode<32>(a, n_work, variant, s);
+    case 64: return launch_decode<64>(a, n_work, variant, s);
+    case 128: return launch_decode<128>(a, n_work, variant, s);
     default: return fail(KVMIX_EINVAL, "decode supports head_dim 32, 64, 128");
   }
 }
