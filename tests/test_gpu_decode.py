@@ -1,0 +1,263 @@
+"""K2 split-K mixed INT2/INT4 decode attention on the GPU vs the reference
+flash_decode (golden outputs) and the oracle restatement: within the north_star
+tolerance (atol 2e-3, rtol 1e-2 vs fp32 dequant-attention), plus size-independent
+properties at the Qwen3-VL-32B shape (32K tokens, 64 q / 8 kv heads)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_17170_b200 as kv
+from oracle import attention as oatt
+from oracle import pool as opool
+
+from conftest import rand_kv
+
+pytestmark = pytest.mark.gpu
+ATOL, RTOL = 2e-3, 1e-2
+
+
+def close(out, ref, atol=ATOL, rtol=RTOL):
+    err = np.abs(np.asarray(out, np.float64) - ref)
+    return bool(np.all(err <= atol + rtol * np.abs(ref))), float(err.max())
+
+
+def build(seed, n, n_kv, d, frac, L=1, headroom=64):
+    rng = np.random.default_rng(seed)
+    bits = np.where(rng.random(n) < frac, 2, 4)
+    k, v = rand_kv(seed, L, n, n_kv, d)
+    offset = -(-int((bits == 2).sum()) // 32) * 32
+    cfg = kv.PoolConfig(total_slots=offset + n + headroom, offset=offset, n_layers=L, n_kv_heads=n_kv, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    t = pool.alloc("req", bits)
+    pool.write_prefill(t, k, v)
+    pool.partition(t)
+    op = opool.OraclePool(opool.Config(cfg.total_slots, cfg.offset, L, n_kv, d))
+    op.alloc("req", bits)
+    op.write_prefill("req", k, v)
+    op.partition("req")
+    return pool, t, op, k, v, bits
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_golden_reference_outputs(cuda, golden, i):
+    d, n_kv, H, n, total, offset = (int(x) for x in golden["dec_meta"][i])
+    pool = kv.MixedPrecisionPool(kv.PoolConfig(total_slots=total, offset=offset, n_layers=1, n_kv_heads=n_kv,
+                                               head_dim=d))
+    t = pool.alloc("req", golden[f"dec{i}_bits"])
+    pool.write_prefill(t, golden[f"dec{i}_keys"].astype(np.float32), golden[f"dec{i}_values"].astype(np.float32))
+    pool.partition(t)
+    ok, err = close(kv.flash_decode(golden[f"dec{i}_q"], t, pool.view(0)), golden[f"dec{i}_out"])
+    assert ok, err
+
+
+def test_random_instances_vs_oracle(cuda):
+    """test_acceptance.py:139-160 shape: 200 random instances, d in {32, 64, 128}, GQA 1..8."""
+    rng = np.random.default_rng(103)
+    worst = 0.0
+    for i in range(200):
+        d = int(rng.choice([32, 64, 128]))
+        n_kv = int(rng.choice([1, 2, 4]))
+        H = n_kv * int(rng.choice([1, 2, 4, 8]))
+        n = int(rng.integers(1, 1200))
+        pool, t, op, *_ = build(1000 + i, n, n_kv, d, float(rng.uniform(0, 1)))
+        q = rng.standard_normal((H, d)).astype(np.float32)
+        ref = oatt.flash_decode_pool(q, op, "req", 0)
+        ok, err = close(kv.flash_decode(q, t, pool.view(0)), ref)
+        worst = max(worst, err)
+        assert ok, (i, d, n_kv, H, n, err)
+        # the CUDA-core variant is an fp32 restatement: much tighter
+        ok2, err2 = close(kv.flash_decode(q, t, pool.view(0), variant=1), ref, atol=1e-5, rtol=1e-5)
+        assert ok2, (i, err2)
+    print(f"worst abs err over 200 instances: {worst:.2e}")
+
+
+def test_edge_cases(cuda):
+    rng = np.random.default_rng(0)
+    for n, frac in [(1, 0.0), (32, 1.0), (33, 1.0), (31, 1.0), (64, 0.5), (1000, 1.0), (1000, 0.0)]:
+        pool, t, op, *_ = build(n, n, 2, 128, frac)
+        q = rng.standard_normal((16, 128)).astype(np.float32)
+        ok, err = close(kv.flash_decode(q, t, pool.view(0)), oatt.flash_decode_pool(q, op, "req", 0))
+        assert ok, (n, frac, err)
+
+
+def test_split_invariance_and_validation(cuda):
+    pool, t, op, *_ = build(19, 500, 2, 64, 0.7)
+    q = np.random.default_rng(20).standard_normal((4, 64)).astype(np.float32)
+    outs = [kv.flash_decode(q, t, pool.view(0), split_len=s) for s in (1, 7, 32, 128, 512)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    qd = torch.as_tensor(q, device=cuda)[None]
+    ref = outs[0]
+    for S in range(1, 9):
+        b = kv.DecodeBatch(pool, ["req"], n_q_heads=4, splits=S)
+        o = kv.flash_decode_batched(qd, b, 0).cpu().numpy()[0]
+        assert np.allclose(o, ref, rtol=1e-4, atol=1e-5), S
+    with pytest.raises(kv.ValidationError):
+        kv.flash_decode(q, t, pool.view(0), split_len=0)
+    with pytest.raises(kv.ValidationError):
+        kv.flash_decode(q[0], t, pool.view(0))
+    with pytest.raises(kv.ValidationError):
+        kv.flash_decode(np.zeros((3, 64), np.float32), t, pool.view(0))
+    t2 = pool.alloc("mixed", np.array([4] * 8 + [2] * 32))
+    k, v = rand_kv(22, 1, 40, 2, 64)
+    pool.write_prefill(t2, k, v)
+    with pytest.raises(kv.ValidationError, match="not partitioned"):
+        kv.flash_decode(q, t2, pool.view(0))
+    empty = kv.PageTable("e", [], partitioned=True)
+    with pytest.raises(kv.ValidationError, match="empty"):
+        kv.flash_decode(q, empty, pool.view(0))
+
+
+def test_batched_mixed_lengths_and_dtypes(cuda):
+    L, n_kv, d, H = 2, 4, 128, 32
+    rng = np.random.default_rng(7)
+    lens = [1, 31, 32, 100, 2000, 4321]
+    cfg = kv.PoolConfig(total_slots=20000, offset=12000, n_layers=L, n_kv_heads=n_kv, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(20000, 12000, L, n_kv, d))
+    rids = []
+    for r, n in enumerate(lens):
+        bits = np.where(rng.random(n) < 0.8, 2, 4)
+        k, v = rand_kv(r, L, n, n_kv, d)
+        t = pool.alloc(f"r{r}", bits)
+        op.alloc(f"r{r}", bits)
+        pool.write_prefill(t, k, v)
+        op.write_prefill(f"r{r}", k, v)
+        pool.partition(t)
+        op.partition(f"r{r}")
+        rids.append(f"r{r}")
+    batch = kv.DecodeBatch(pool, rids, n_q_heads=H)
+    q = torch.randn(len(lens), H, d, device=cuda)
+    for layer in range(L):
+        for qd, od in [(torch.float32, torch.float32), (torch.bfloat16, torch.bfloat16),
+                       (torch.float16, torch.float32)]:
+            qq = q.to(qd)
+            out = torch.empty(len(lens), H, d, dtype=od, device=cuda)
+            kv.flash_decode_batched(qq, batch, layer, out=out)
+            for r in range(len(lens)):
+                ref = oatt.flash_decode_pool(qq[r].float().cpu().numpy(), op, f"r{r}", layer)
+                atol = ATOL + (4e-3 if od == torch.bfloat16 else 0.0)  # bf16 output rounding
+                ok, err = close(out[r].float().cpu().numpy(), ref, atol=atol)
+                assert ok, (layer, qd, od, r, err)
+
+
+def test_decode_after_append(cuda):
+    pool, t, op, *_ = build(5, 700, 2, 128, 0.8, L=2, headroom=128)
+    rng = np.random.default_rng(1)
+    for _ in range(40):
+        kk = rng.standard_normal((2, 2, 128)).astype(np.float32)
+        vv = rng.standard_normal((2, 2, 128)).astype(np.float32)
+        a = pool.append_decode_token("req", kk, vv)
+        s = op.pop_decode_slot("req")
+        op.write_decode(s, kk, vv)
+        assert a.index == s
+    q = rng.standard_normal((16, 128)).astype(np.float32)
+    for layer in range(2):
+        ok, err = close(kv.flash_decode(q, t, pool.view(layer)), oatt.flash_decode_pool(q, op, "req", layer))
+        assert ok, err
+
+
+def test_cuda_graph_capture(cuda):
+    pool, t, op, *_ = build(8, 3000, 2, 128, 0.8)
+    batch = kv.DecodeBatch(pool, ["req"], n_q_heads=16)
+    q = torch.randn(1, 16, 128, device=cuda)
+    out = torch.empty_like(q)
+    kv.flash_decode_batched(q, batch, 0, out=out)
+    eager = out.clone()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            kv.flash_decode_batched(q, batch, 0, out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+
+
+# ---- full-size (Qwen3-VL-32B layer shape, 32K tokens) size-independent properties ----------
+def big_pool(seed, n=32768, n_kv=8, d=128, frac=0.83, k_fn=None):
+    rng = np.random.default_rng(seed)
+    bits = np.where(rng.random(n) < frac, 2, 4)
+    cfg = kv.PoolConfig(total_slots=n + 64, offset=int((bits == 2).sum()) // 32 * 32, n_layers=1, n_kv_heads=n_kv,
+                        head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    t = pool.alloc("big", bits)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    k = torch.randn(1, n, n_kv, d, device="cuda", generator=gen) if k_fn is None else k_fn(n, n_kv, d)
+    v = torch.randn(1, n, n_kv, d, device="cuda", generator=gen)
+    pool.write_prefill(t, k.to(torch.bfloat16), v.to(torch.bfloat16))
+    pool.partition(t)
+    return pool, t, v
+
+
+def test_fullsize_tensor_core_vs_cuda_core(cuda):
+    pool, t, _ = big_pool(1)
+    b = kv.DecodeBatch(pool, ["big"], n_q_heads=64)
+    q = torch.randn(1, 64, 128, device=cuda)
+    a = kv.flash_decode_batched(q, b, 0)
+    c = kv.flash_decode_batched(q, b, 0, variant=1)
+    err = (a - c).abs()
+    assert bool((err <= ATOL + RTOL * c.abs()).all()), float(err.max())
+
+
+def test_fullsize_uniform_keys_give_mean_value(cuda):
+    """Identical keys -> uniform attention -> output = mean of the dequantized values."""
+    pool, t, _ = big_pool(2, k_fn=lambda n, h, d: torch.ones(1, n, h, d, device="cuda").mul_(0.5))
+    b = kv.DecodeBatch(pool, ["big"], n_q_heads=64)
+    q = torch.randn(1, 64, 128, device=cuda)
+    out = kv.flash_decode_batched(q, b, 0)[0]
+    kd, vd = pool._gather_dev(t.slots, 0)  # K5 gather-dequant (checked bit-exact in test_gpu_pool)
+    mean = vd.mean(dim=0)  # [Hkv, d]
+    expect = mean.repeat_interleave(8, dim=0)
+    assert torch.allclose(out, expect, atol=1e-4, rtol=1e-3), float((out - expect).abs().max())
+
+
+def test_fullsize_page_order_invariance(cuda):
+    pool, t, _ = big_pool(3, n=8192)
+    q = torch.randn(1, 64, 128, device=cuda)
+    b1 = kv.DecodeBatch(pool, ["big"], n_q_heads=64)
+    o1 = kv.flash_decode_batched(q, b1, 0)
+    s = t.slots
+    n2 = int((s < pool.config.offset).sum())
+    pages = s[:n2].reshape(-1, 32)[::-1].reshape(-1)
+    perm = np.concatenate([pages, s[n2:][::-1]])
+    b2 = kv.DecodeBatch(pool, n_q_heads=64, tables=[perm])
+    o2 = kv.flash_decode_batched(q, b2, 0)
+    assert torch.allclose(o1, o2, atol=1e-5, rtol=1e-4)
+
+
+def test_fullsize_value_linearity(cuda):
+    """Scaling V by 2 doubles every fp16 scale/zero exactly, so the output doubles."""
+    torch.manual_seed(0)
+    n, h, d = 16384, 8, 128
+    bits = np.where(np.random.default_rng(4).random(n) < 0.8, 2, 4)
+    k = torch.randn(1, n, h, d, device=cuda)
+    v = torch.randn(1, n, h, d, device=cuda)
+    outs = []
+    for mult in (1.0, 2.0):
+        cfg = kv.PoolConfig(total_slots=n + 32, offset=int((bits == 2).sum()) // 32 * 32, n_layers=1,
+                            n_kv_heads=h, head_dim=d)
+        pool = kv.MixedPrecisionPool(cfg)
+        t = pool.alloc("r", bits)
+        pool.write_prefill(t, k, v * mult)
+        pool.partition(t)
+        b = kv.DecodeBatch(pool, ["r"], n_q_heads=64)
+        outs.append(kv.flash_decode_batched(torch.ones(1, 64, d, device=cuda) * 0.1, b, 0))
+    assert torch.allclose(outs[1], 2 * outs[0], atol=1e-4, rtol=1e-3)
+
+
+def test_merge_partials_gpu(cuda):
+    rng = np.random.default_rng(16)
+    parts = [kv.SplitPartial(acc=rng.standard_normal(8).astype(np.float32), lse=float(rng.uniform(-5, 5)),
+                             max_logit=float(rng.uniform(-5, 5))) for _ in range(5)]
+    a = kv.merge_partials(parts)
+    b = oatt.merge([(p.acc, p.lse, p.max_logit) for p in parts])
+    assert np.allclose(a, b, rtol=1e-5)
+    big = kv.SplitPartial(acc=np.ones(4, np.float32) * 3, lse=1000.0, max_logit=1000.0)
+    tiny = kv.SplitPartial(acc=np.ones(4, np.float32), lse=-1000.0, max_logit=-1000.0)
+    assert np.allclose(kv.merge_partials([big, tiny]), 3.0, atol=1e-5)
+    with pytest.raises(kv.ValidationError):
+        kv.merge_partials([])

@@ -1,0 +1,195 @@
+"""Pool data plane on the GPU: write_prefill / append / gather produce exactly the
+oracle's device image (every reference payload at its slot address) with the
+reference's page indices; error behaviour and accounting follow pool.py."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2605_17170_b200 as kv
+from oracle import pool as opool
+
+from conftest import rand_kv
+
+pytestmark = pytest.mark.gpu
+
+
+def pool_images(pool):
+    L, H = pool.config.n_layers, pool.config.n_kv_heads
+    i2 = pool.int2_pool[: L * H * pool.n_pages * pool.page_stride].view(L, H, pool.n_pages, pool.page_stride)
+    i4 = pool.int4_pool[: L * H * pool.n_int4 * pool.slot_stride].view(L, H, pool.n_int4, pool.slot_stride)
+    return i2.cpu().numpy(), i4.cpu().numpy()
+
+
+def assert_same_image(pool, op):
+    i2, i4 = pool_images(pool)
+    assert np.array_equal(i2[op.page_written], op.int2[op.page_written])
+    assert np.array_equal(i4[op.slot_written], op.int4[op.slot_written])
+
+
+@pytest.mark.parametrize("d,dtype", [(32, torch.float32), (64, torch.bfloat16), (128, torch.float32),
+                                     (128, torch.bfloat16), (128, torch.float16), (256, torch.float32)])
+def test_prefill_bytes_match_oracle(cuda, d, dtype):
+    L, H = 2, 2
+    cfg = kv.PoolConfig(total_slots=3000, offset=1600, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(3000, 1600, L, H, d))
+    rng = np.random.default_rng(d)
+    for r in range(5):
+        n = int(rng.integers(1, 500))
+        bits = rng.choice([2, 4], size=n, p=[0.8, 0.2])
+        k, v = rand_kv(r, L, n, H, d)
+        kt = torch.as_tensor(k, device=cuda).to(dtype)
+        vt = torch.as_tensor(v, device=cuda).to(dtype)
+        t = pool.alloc(f"r{r}", bits)
+        assert t.slots.tolist() == op.alloc(f"r{r}", bits)
+        pool.write_prefill(t, kt, vt)
+        op.write_prefill(f"r{r}", kt.float().cpu().numpy(), vt.float().cpu().numpy())  # exact upcast
+        if r == 2:
+            pool.free("r1")
+            op.free("r1")
+    torch.cuda.synchronize()
+    assert_same_image(pool, op)
+    pool.check_invariants()
+
+
+def test_gather_and_read_slot(cuda):
+    L, H, d = 2, 2, 64
+    cfg = kv.PoolConfig(total_slots=600, offset=320, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(600, 320, L, H, d))
+    bits = np.array([2] * 70 + [4] * 30 + [2] * 40)
+    k, v = rand_kv(9, L, bits.size, H, d)
+    t = pool.alloc("r", bits)
+    op.alloc("r", bits)
+    pool.write_prefill(t, k, v)
+    op.write_prefill("r", k, v)
+    for layer in range(L):
+        kg, vg = pool.view(layer).gather(t.entries)
+        ko, vo = op.gather(t.slots, layer)
+        assert np.array_equal(kg, ko) and np.array_equal(vg, vo)
+    for i in (0, 31, 75, 120, 139):
+        for h in range(H):
+            ks, vs = pool.read_slot(t.entries[i], 1, h)
+            ko, vo = op.gather([t.slots[i]], 1)
+            assert np.array_equal(ks, ko[0, h]) and np.array_equal(vs, vo[0, h])
+
+
+def test_append_decode_token(cuda):
+    L, H, d = 3, 2, 128
+    cfg = kv.PoolConfig(total_slots=256, offset=128, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(256, 128, L, H, d))
+    bits = np.array([2] * 64 + [4] * 5)
+    k, v = rand_kv(3, L, bits.size, H, d)
+    t = pool.alloc("r", bits)
+    op.alloc("r", bits)
+    pool.write_prefill(t, k, v)
+    op.write_prefill("r", k, v)
+    with pytest.raises(kv.ValidationError):
+        pool.append_decode_token("r", k[:, 0], v[:, 0])  # table not partitioned yet
+    pool.partition(t)
+    op.partition("r")
+    rng = np.random.default_rng(0)
+    for _ in range(7):
+        kk = rng.standard_normal((L, H, d)).astype(np.float32)
+        vv = rng.standard_normal((L, H, d)).astype(np.float32)
+        a = pool.append_decode_token("r", kk, vv)
+        s = op.pop_decode_slot("r")
+        op.write_decode(s, kk, vv)
+        assert a.index == s and not pool.is_int2(a) and t.slots[-1] == s
+    assert_same_image(pool, op)
+    # batched append (one token per request, all layers) == per-request appends
+    kb = torch.as_tensor(rng.standard_normal((1, L, H, d)), dtype=torch.float32, device=cuda)
+    slots = pool.append_decode_tokens(["r"], kb, kb)
+    s = op.pop_decode_slot("r")
+    op.write_decode(s, kb[0].cpu().numpy(), kb[0].cpu().numpy())
+    assert slots.tolist() == [s]
+    assert_same_image(pool, op)
+    pool.check_invariants()
+
+
+def test_write_page_and_token(cuda):
+    cfg = kv.PoolConfig(total_slots=256, offset=128, n_layers=2, n_kv_heads=2, head_dim=32)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(256, 128, 2, 2, 32))
+    pool.alloc("r", np.array([2] * 32 + [4]))
+    op.alloc("r", np.array([2] * 32 + [4]))
+    rng = np.random.default_rng(4)
+    keys = rng.standard_normal((32, 32)).astype(np.float32)
+    vals = rng.standard_normal((32, 32)).astype(np.float32)
+    pool.write_page(0, keys, vals, 1, 1)
+    k4 = rng.standard_normal(32).astype(np.float32)
+    pool.write_token(kv.SlotAddress(128), k4, -k4, 0, 1)
+    from oracle import codec
+    i2, i4 = pool_images(pool)
+    exp2 = np.concatenate([codec.encode_key_pages(keys), codec.encode_token_blocks(vals, 2).reshape(-1)])
+    assert np.array_equal(i2[1, 1, 0, : exp2.size], exp2)
+    exp4 = np.concatenate([codec.encode_token_blocks(k4[None], 4)[0], codec.encode_token_blocks(-k4[None], 4)[0]])
+    assert np.array_equal(i4[0, 1, 0, : exp4.size], exp4)
+    with pytest.raises(kv.ValidationError):
+        pool.write_page(0, np.zeros((16, 32)), np.zeros((16, 32)), 0, 0)
+    with pytest.raises(kv.ValidationError):
+        pool.write_token(kv.SlotAddress(0), np.zeros(32), np.zeros(32), 0, 0)
+    with pytest.raises(kv.ValidationError):
+        pool.write_page(5, keys, vals, 0, 0)
+
+
+def test_errors_and_accounting(cuda):
+    cfg = kv.PoolConfig(total_slots=256, offset=128, n_layers=1, n_kv_heads=1, head_dim=32)
+    pool = kv.MixedPrecisionPool(cfg)
+    t = pool.alloc("r", np.array([4]))
+    with pytest.raises(kv.ValidationError):
+        pool.read_slot(t.entries[0], 0, 0)  # read before write
+    k, v = rand_kv(0, 1, 1, 1, 32)
+    pool.write_prefill(t, k, v)
+    addr = t.entries[0]
+    pool.free("r")
+    with pytest.raises(kv.ValidationError):
+        pool.read_slot(addr, 0, 0)
+    with pytest.raises(kv.ValidationError):
+        pool.view(0).gather([kv.SlotAddress(5)])
+    t = pool.alloc("p", np.array([2] * 32 + [4]))
+    k, v = rand_kv(7, 1, 33, 1, 32)
+    pool.write_prefill(t, k, v)
+    assert pool.parameter_overhead_bytes() == 32 * 4 + 32 * 1 * 4 + 2 * 1 * 4  # test_pool.py:285-292
+    bad = np.full((1, 33, 1, 32), np.nan, np.float32)
+    pool.alloc("z", np.array([4] * 33))
+    with pytest.raises(kv.ValidationError, match="finite"):
+        pool.write_prefill(pool.table("z"), bad, bad)
+    tiny = kv.MixedPrecisionPool(kv.PoolConfig(total_slots=32, offset=32, n_layers=1, n_kv_heads=1, head_dim=32))
+    t = tiny.alloc("r", np.array([2] * 32))
+    k, v = rand_kv(5, 1, 32, 1, 32)
+    tiny.write_prefill(t, k, v)
+    tiny.partition(t)
+    with pytest.raises(kv.CapacityError) as e:
+        tiny.append_decode_token("r", np.zeros((1, 1, 32), np.float32), np.zeros((1, 1, 32), np.float32))
+    assert e.value.region == "int4"
+
+
+def test_fuzz_safety(cuda):
+    """test_acceptance.py:304-342 pattern (criterion 9) on the device pool, 2000 ops."""
+    pool = kv.MixedPrecisionPool(kv.PoolConfig(total_slots=512, offset=288, n_layers=1, n_kv_heads=1, head_dim=32))
+    rng = np.random.default_rng(109)
+    live, nid = [], 0
+    z = np.zeros((1, 1, 32), np.float32)
+    for _ in range(2000):
+        a = rng.random()
+        try:
+            if a < 0.45 or not live:
+                bits = rng.choice([2, 4], size=int(rng.integers(1, 80)), p=[0.6, 0.4])
+                t = pool.alloc(f"r{nid}", bits)
+                assert int((t.slots < 288).sum()) == int((bits == 2).sum()) // 32 * 32
+                live.append(f"r{nid}")
+                nid += 1
+            elif a < 0.8:
+                pool.free(live.pop(int(rng.integers(len(live)))))
+            else:
+                rid = live[int(rng.integers(len(live)))]
+                t = pool.partition(pool.table(rid))
+                before = t.slots.tolist()
+                pool.partition(t)
+                assert t.slots.tolist()[: len(before)] == before
+                pool.append_decode_token(rid, z, z)
+        except kv.CapacityError:
+            pass
+        pool.check_invariants()

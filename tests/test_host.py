@@ -1,0 +1,232 @@
+"""Host-side product logic on CPU: the C ABI loads and exports every declared symbol,
+the control plane (allocator, partition, page tables) reproduces the reference's slot
+indices exactly, pool sizing arithmetic, the split planner and error mapping."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2605_17170_b200 as kv
+from paper_2605_17170_b200 import _lib
+from paper_2605_17170_b200.plan import plan_splits
+from paper_2605_17170_b200.pool import csr_tables, split_partitioned
+from oracle import pool as opool
+
+from conftest import GOLDEN, ROOT
+
+
+def host_pool(total, offset, L=1, H=1, d=32):
+    return kv.MixedPrecisionPool(kv.PoolConfig(total_slots=total, offset=offset, n_layers=L, n_kv_heads=H,
+                                               head_dim=d), materialize=False)
+
+
+# ---- C ABI -----------------------------------------------------------------------------------
+def test_abi_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "kvmix_b200.h")).read()
+    declared = set(re.findall(r"\b(kvmix_\w+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    missing = [n for n in declared if not hasattr(_lib.lib, n)]
+    assert not missing, missing
+    assert declared == set(_lib.EXPORTED)
+
+
+def test_abi_strides_and_sizes():
+    for d in (32, 64, 128, 256):
+        assert _lib.lib.kvmix_key_page_payload_bytes(d) == kv.key_page_payload_bytes(d)
+        for b in (2, 4):
+            assert _lib.lib.kvmix_token_block_payload_bytes(d, b) == kv.token_block_payload_bytes(d, b)
+        assert _lib.page_stride(d) % 16 == 0 and _lib.slot_stride(d) % 16 == 0
+        assert _lib.page_stride(d) >= kv.key_page_payload_bytes(d) + 32 * kv.token_block_payload_bytes(d, 2)
+        assert _lib.slot_stride(d) >= 2 * kv.token_block_payload_bytes(d, 4)
+    assert _lib.page_stride(128) == 3072 and _lib.slot_stride(128) == 160
+    assert _lib.lib.kvmix_version().startswith(b"kvmix_b200")
+
+
+def test_abi_validation_without_gpu():
+    # argument validation happens before any CUDA call and maps to ValidationError
+    rc = _lib.lib.kvmix_encode_token_blocks(None, 1, 33, 2, None, 36, None, None)
+    with pytest.raises(kv.ValidationError):
+        _lib.check(rc)
+    rc = _lib.lib.kvmix_flash_decode(None, 0, None, 0, None, None, 1, 1, 0, 3, 128, 8, 1, None, None, None, None,
+                                     None, 3, 1.0, 0, None)
+    with pytest.raises(kv.ValidationError, match="multiple"):
+        _lib.check(rc)
+
+
+# ---- control plane vs the oracle and the reference trace --------------------------------------
+def test_alloc_trace_matches_reference():
+    tr = json.load(open(os.path.join(GOLDEN, "alloc_trace.json")))
+    p = host_pool(tr["total_slots"], tr["offset"])
+    for rec in tr["ops"]:
+        try:
+            if rec["op"] == "alloc":
+                t = p.alloc(rec["rid"], np.array(rec["bits"]))
+                assert t.slots.tolist() == rec["slots"]
+            elif rec["op"] == "free":
+                p.free(rec["rid"])
+            else:
+                t = p.partition(p.table(rec["rid"]))
+                slot = p._free_int4[-1] if p._free_int4 else None
+                # slot bookkeeping of append_decode_token without the device write
+                if not p._free_int4:
+                    raise kv.CapacityError("INT4 region exhausted during decode", region="int4")
+                s = p._free_int4.pop()
+                p._owner[s] = p._rid_index[rec["rid"]]
+                t._set_slots(np.append(t.slots, s))
+                assert s == rec["slot"] == slot
+                assert t.slots.tolist() == rec["slots"]
+            assert "capacity" not in rec
+        except kv.CapacityError as e:
+            assert e.region == rec["capacity"]
+        assert p._free_pages == rec["free_pages"]
+        assert p._free_int4 == rec["free_int4"]
+        p.check_invariants()
+
+
+def test_alloc_fuzz_vs_oracle():
+    rng = np.random.default_rng(42)
+    p = host_pool(2048, 1024)
+    o = opool.OraclePool(opool.Config(2048, 1024, 1, 1, 32), data_plane=False)
+    live = []
+    for i in range(400):
+        a = rng.random()
+        if a < 0.5 or not live:
+            bits = rng.choice([2, 4], size=int(rng.integers(1, 200)), p=[0.75, 0.25])
+            try:
+                s = p.alloc(f"r{i}", bits).slots.tolist()
+            except kv.CapacityError as e:
+                with pytest.raises(opool.OracleError) as oe:
+                    o.alloc(f"r{i}", bits)
+                assert oe.value.region == e.region
+                continue
+            assert s == o.alloc(f"r{i}", bits)
+            live.append(f"r{i}")
+        elif a < 0.8:
+            rid = live.pop(int(rng.integers(len(live))))
+            p.free(rid)
+            o.free(rid)
+        else:
+            rid = live[int(rng.integers(len(live)))]
+            assert p.partition(p.table(rid)).slots.tolist() == o.partition(rid)
+        assert p._free_pages == o.free_pages and p._free_int4 == o.free_int4
+        p.check_invariants()
+
+
+def test_alloc_semantics():
+    p = host_pool(256, 128)
+    bits = np.array([2] * 32 + [4] * 10)
+    t = p.alloc("r", bits)
+    assert t.slots[:32].tolist() == list(range(32)) and t.slots[32] == 128       # lowest first
+    t2 = p.alloc("s", np.array([2] * 40))                                          # residual -> INT4
+    assert int((t2.slots < 128).sum()) == 32 and p.live_counts() == (64, 18)
+    with pytest.raises(kv.ValidationError):
+        p.alloc("r", np.array([4]))
+    with pytest.raises(kv.ValidationError):
+        p.alloc("x", np.array([3]))
+    first = p.alloc("a", np.array([4] * 3)).slots.tolist()
+    p.free("a")
+    assert p.alloc("b", np.array([4] * 3)).slots.tolist() == first[::-1]           # LIFO reuse
+    with pytest.raises(kv.ValidationError):
+        p.free("a")
+    small = host_pool(64, 32)
+    with pytest.raises(kv.CapacityError) as e:
+        small.alloc("r", np.array([2] * 64))
+    assert e.value.region == "int2"
+    with pytest.raises(kv.CapacityError) as e:
+        small.alloc("r", np.array([4] * 33))
+    assert e.value.region == "int4"
+
+
+def test_partition_stable_idempotent():
+    p = host_pool(256, 128)
+    t = p.alloc("r", np.array([4, 2, 4] + [2] * 31 + [4]))
+    orig = t.slots.copy()
+    p.partition(t)
+    assert t.slots.tolist() == orig[orig < 128].tolist() + orig[orig >= 128].tolist()
+    snap = t.slots.tolist()
+    p.partition(t)
+    assert t.slots.tolist() == snap
+    assert [a.index for a in t.entries] == snap
+    pages, int4 = split_partitioned(t.slots, 128)
+    assert pages.tolist() == [orig[orig < 128][0] // 32] and int4.tolist() == (orig[orig >= 128] - 128).tolist()
+
+
+def test_split_partitioned_rejects():
+    with pytest.raises(kv.ValidationError, match="not partitioned"):
+        split_partitioned(np.array([200, 0, 1]), 128)
+    with pytest.raises(kv.ValidationError, match="page-granular"):
+        split_partitioned(np.array([0, 1, 2]), 128)
+
+
+def test_init_pool_offsets():
+    assert kv.init_pool(2.5, 1000, 1, 1, 32).offset == 736
+    assert kv.init_pool(2.7, 3200, 1, 1, 32).offset == 2080
+    assert kv.init_pool(2.5, 3200, 1, 1, 32).offset == 2400
+    assert kv.init_pool(4.0, 320, 1, 1, 32).offset == 0
+    assert kv.init_pool(2.0, 320, 1, 1, 32).offset == 320
+    for b in (2.0, 2.3, 3.1, 4.0):
+        assert kv.init_pool(b, 999, 1, 1, 32).offset % 32 == 0
+    with pytest.raises(kv.ValidationError):
+        kv.init_pool(1.5, 320, 1, 1, 32)
+    with pytest.raises(kv.ValidationError):
+        kv.PoolConfig(total_slots=128, offset=30, n_layers=1, n_kv_heads=1, head_dim=32)
+
+
+def test_capacity_headroom():
+    dims = dict(head_dim=128, n_layers=32, n_kv_heads=8)
+    n = 11_000
+    assert kv.capacity_tokens(n * kv.baseline_bytes_per_token(**dims), 2.7, **dims) / n >= 4.0
+    assert kv.bytes_per_token(128, 1, 1, 2) == 96 and kv.bytes_per_token(128, 1, 1, 4) == 160
+
+
+def test_stats_accounting():
+    p = host_pool(256, 128)
+    p.alloc("r", np.array([2] * 64 + [4] * 36))
+    st = p.stats()
+    assert st["realized_avg_bitwidth"] == pytest.approx((2 * 64 + 4 * 36) / 100)
+    assert st["int2"]["live"] == 64 and st["int4"]["live"] == 36
+
+
+# ---- split planner --------------------------------------------------------------------------
+@pytest.mark.parametrize("B,Hkv", [(1, 2), (16, 8), (64, 8), (3, 1)])
+def test_plan_covers_every_tile(B, Hkv):
+    rng = np.random.default_rng(B)
+    npg = rng.integers(0, 1200, B)
+    n4 = rng.integers(0, 5000, B)
+    n4[npg == 0] += 1
+    work, S = plan_splits(npg, n4, Hkv, 3072, 160)
+    assert 1 <= S <= 8 and work.shape == (B * Hkv * S, 4)
+    w = work.reshape(B, Hkv, S, 4)
+    tiles = npg + (n4 + 31) // 32
+    for b in range(B):
+        for h in range(Hkv):
+            assert (w[b, h, :, 0] == b * Hkv + h).all()
+            assert w[b, h, 0, 1] == 0 and w[b, h, -1, 2] == tiles[b]
+            assert (w[b, h, 1:, 1] == w[b, h, :-1, 2]).all() and (w[b, h, :, 2] >= w[b, h, :, 1]).all()
+
+
+def test_plan_byte_balance():
+    work, S = plan_splits(np.array([1000] * 16), np.array([6000] * 16), 8, 3072, 160, splits=4)
+    w = work.reshape(16, 8, 4, 4)[0, 0]
+    sizes = []
+    for lo, hi in w[:, 1:3]:
+        b = sum(3072 if t < 1000 else 32 * 160 for t in range(lo, hi))
+        sizes.append(b)
+    assert max(sizes) / min(sizes) < 1.05
+
+
+def test_csr_tables_cpu():
+    t = csr_tables([np.array([3, 1], np.int32), np.array([], np.int32)], [np.array([5]), np.array([0, 1, 2])],
+                   "cpu")
+    assert t["page_indptr"].tolist() == [0, 2, 2] and t["int4_indptr"].tolist() == [0, 1, 4]
+    assert t["n_pages"].tolist() == [2, 0] and t["n_int4"].tolist() == [1, 3]
+
+
+def test_error_mapping():
+    with pytest.raises(kv.KvmixError):
+        _lib.check(-5)
+    with pytest.raises(kv.CapacityError):
+        _lib.check(-3)
+    _lib.check(0)
