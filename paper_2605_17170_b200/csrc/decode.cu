@@ -258,9 +258,19 @@ __device__ __forceinline__ void pv_zeros(Acc<D>& acc, uint32_t zA0, uint32_t zA1
   mma16816_b64(acc.zs, zA, zA0, zB, zB0, pack_b64(bP0, bP1));
 }
 
+// Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).  b2: INT2 key
+// pages, chunk i, lane q pairs channels (16i+4q+{0,1}) / (16i+4q+{2,3}); b4: INT4 keys,
+// chunk 2j+s pairs (32j+8q+{0,4}) / ({1,5}) (s=0) or ({2,6}) / ({3,7}) (s=1).  With LO
+// (fp32 q), *lo hold q - fp16(q) so the bias and INT4 products see ~22-bit q.
+template <int D, bool LO>
+struct QFrag {
+  uint64_t b2[D / 16], b4[D / 16];
+  uint64_t b2lo[LO ? D / 16 : 1], b4lo[LO ? D / 16 : 1];
+};
+
 // ---------------------------------- INT2 page tile ----------------------------------
-template <int D>
-__device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const uint64_t (&qb2)[D / 16],
+template <int D, bool LO>
+__device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
                                           int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
   const int g = lane >> 2, q = lane & 3;
@@ -275,18 +285,21 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
     const uint32_t r1 = prmt(ld_s32(kb, 128 * i), ld_s32(kb, 128 * i + 8), selK);
     const uint32_t r2 = prmt(ld_s32(kb, 128 * i + 16), ld_s32(kb, 128 * i + 24), selK);
     const uint4 pv = *reinterpret_cast<const uint4*>(pb + 64 * i);
-    const uint64_t qi = qb2[i];
+    const uint64_t qi = qf.b2[i];
     const uint64_t qs = pack_b64(hmul2u(lo32(qi), prmt(pv.x, pv.y, 0x5410)), hmul2u(hi32(qi), prmt(pv.z, pv.w, 0x5410)));
     const uint32_t z1 = prmt(pv.x, pv.y, 0x7632), z2 = prmt(pv.z, pv.w, 0x7632);
     mma16816_b64(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qs);
     mma16816_b64(c1, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qs);
     // bias rows g carry sum_c q_c z_c; rows g+8 (cb[2], cb[3]) are don't-care filler
     mma16816_b64(cb, z1, r1, z2, r2, qi);
+    if constexpr (LO) mma16816_b64(cb, z1, r1, z2, r2, qf.b2lo[i]);
   }
-  // undo 2^(2k-10) per token row (k = token position inside its code byte)
-  const float sv[8] = {fmaf(c0[0], 1024.f, cb[0]), fmaf(c0[1], 1024.f, cb[1]), fmaf(c0[2], 256.f, cb[0]),
-                       fmaf(c0[3], 256.f, cb[1]),  fmaf(c1[0], 64.f, cb[0]),   fmaf(c1[1], 64.f, cb[1]),
-                       fmaf(c1[2], 16.f, cb[0]),   fmaf(c1[3], 16.f, cb[1])};
+  // undo 2^(2k-10) per token row (k = token position inside its code byte), apply scale*log2(e)
+  const float b0 = cb[0] * qscale, b1 = cb[1] * qscale;
+  const float sv[8] = {fmaf(c0[0], 1024.f * qscale, b0), fmaf(c0[1], 1024.f * qscale, b1),
+                       fmaf(c0[2], 256.f * qscale, b0),  fmaf(c0[3], 256.f * qscale, b1),
+                       fmaf(c1[0], 64.f * qscale, b0),   fmaf(c1[1], 64.f * qscale, b1),
+                       fmaf(c1[2], 16.f * qscale, b0),   fmaf(c1[3], 16.f * qscale, b1)};
   uint32_t bP[2][2];
   softmax_tile<D>(sv, st, acc, bP);
   // PV: k-step ks, pair A tokens (4q+2ks, 16+4q+2ks), pair B = pair A + 1
@@ -326,9 +339,9 @@ __device__ __forceinline__ uint32_t int4_deq(uint32_t field16, uint32_t s16, uin
   return hfma2u(hsub2u(field16, MAGIC), s16, zz);  // (code/16) * 16s + z
 }
 
-template <int D, bool FULL>
-__device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const uint64_t (&qb4)[D / 16],
-                                          int lane, Softmax& st, Acc<D>& acc) {
+template <int D, bool FULL, bool LO>
+__device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const QFrag<D, LO>& qf,
+                                          float qscale, int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
   constexpr int S = C::SS;
   const int g = lane >> 2, q = lane & 3;
@@ -353,13 +366,21 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
       e[r][2] = int4_deq(lop_and_or(w >> 2, 0x03C003C0u, MAGIC), s16, zz);
       e[r][3] = int4_deq(lop_and_or(w >> 6, 0x03C003C0u, MAGIC), s16, zz);
     }
-    const uint64_t qa = qb4[2 * j], qc = qb4[2 * j + 1];
+    const uint64_t qa = qf.b4[2 * j], qc = qf.b4[2 * j + 1];
     mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], qa);
     mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], qc);
     mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], qa);
     mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], qc);
+    if constexpr (LO) {
+      const uint64_t la = qf.b4lo[2 * j], lc = qf.b4lo[2 * j + 1];
+      mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], la);
+      mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], lc);
+      mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], la);
+      mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], lc);
+    }
   }
-  float sv[8] = {c0[0], c0[1], c0[2], c0[3], c1[0], c1[1], c1[2], c1[3]};
+  float sv[8] = {c0[0] * qscale, c0[1] * qscale, c0[2] * qscale, c0[3] * qscale,
+                 c1[0] * qscale, c1[1] * qscale, c1[2] * qscale, c1[3] * qscale};
   if (!FULL) {
     if (beta >= nv) sv[0] = sv[1] = -INFINITY;
     if (beta + 8 >= nv) sv[2] = sv[3] = -INFINITY;
@@ -421,7 +442,7 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
   }
 }
 
-template <int D, bool COMPUTE = true, bool MEMORY = true>
+template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false>
 __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -482,20 +503,25 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   }
   int meta_next = load_meta(STAGES);
 
-  // ---- Q fragments (B operand of QK), fp16, pre-scaled by scale*log2(e) ----
-  // qb2: INT2 key pages, chunk i, lane q: pairs (16i+4q+{0,1}) and (16i+4q+{2,3}).
-  // qb4: INT4 keys, chunk 2j+s pairs channels (32j+8q+{0,4}/{1,5}) (s=0) or ({2,6}/{3,7}) (s=1).
-  uint64_t qb2[C::NCH], qb4[C::NCH];
+  // ---- Q fragments (see QFrag) ----
+  QFrag<D, LO> qf;
   {
     const bool hv = g < a.gq;
     const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
-    auto qv = [&](int c) { return hv ? load_q(a, qrow + c) * a.qscale : 0.f; };
+    auto qv = [&](int c) { return hv ? load_q(a, qrow + c) : 0.f; };
+    auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
 #pragma unroll
     for (int i = 0; i < C::NCH; ++i) {
       const int c2 = 16 * i + 4 * q;
-      qb2[i] = pack_b64(pack_h2(qv(c2), qv(c2 + 1)), pack_h2(qv(c2 + 2), qv(c2 + 3)));
-      const int base = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
-      qb4[i] = pack_b64(pack_h2(qv(base + 0), qv(base + 4)), pack_h2(qv(base + 1), qv(base + 5)));
+      const int b4 = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
+      const float x0 = qv(c2), x1 = qv(c2 + 1), x2 = qv(c2 + 2), x3 = qv(c2 + 3);
+      const float y0 = qv(b4), y1 = qv(b4 + 4), y2 = qv(b4 + 1), y3 = qv(b4 + 5);
+      qf.b2[i] = pack_b64(pack_h2(x0, x1), pack_h2(x2, x3));
+      qf.b4[i] = pack_b64(pack_h2(y0, y1), pack_h2(y2, y3));
+      if constexpr (LO) {
+        qf.b2lo[i] = pack_b64(pack_h2(lo(x0), lo(x1)), pack_h2(lo(x2), lo(x3)));
+        qf.b4lo[i] = pack_b64(pack_h2(lo(y0), lo(y1)), pack_h2(lo(y2), lo(y3)));
+      }
     }
   }
 
@@ -516,11 +542,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
     } else if (t < u.npg) {
-      int2_tile<D>(buf, qb2, lane, st, acc);
+      int2_tile<D, LO>(buf, qf, a.qscale, lane, st, acc);
     } else {
       const int nv = min(32, u.n4 - 32 * (t - u.npg));
-      if (nv == 32) int4_tile<D, true>(buf, 32, qb4, lane, st, acc);
-      else int4_tile<D, false>(buf, nv, qb4, lane, st, acc);
+      if (nv == 32) int4_tile<D, true, LO>(buf, 32, qf, a.qscale, lane, st, acc);
+      else int4_tile<D, false, LO>(buf, nv, qf, a.qscale, lane, st, acc);
     }
     __syncwarp();
     if (MEMORY && k + STAGES < nmine) {
@@ -684,7 +710,10 @@ static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_work, int sme
 template <int D>
 static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaStream_t s) {
   switch (variant) {
-    case 0: return launch_kernel(decode_mma_kernel<D, true, true>, a, n_work, Cfg<D>::SMEM, s);
+    case 0:
+      // fp32 q carries bits fp16 cannot hold: add the q - fp16(q) correction MMAs
+      if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_mma_kernel<D, true, true, true>, a, n_work, Cfg<D>::SMEM, s);
+      return launch_kernel(decode_mma_kernel<D, true, true, false>, a, n_work, Cfg<D>::SMEM, s);
     case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, 0, s);
     case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
     default: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
