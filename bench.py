@@ -146,70 +146,83 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------
 # CPU baseline: the oracle port (numpy restatement of the reference flash_decode,
 # attention.py:175-218) on host cores; one worker per core over (request, layer) units.
+_CPU_CACHE: dict = {}
+
+
 def _cpu_unit(args):
+    """Time one (request, layer) flash_decode of the oracle port; the oracle pool of each
+    (ctx, seed) is built once per worker process (not timed)."""
     ctx, hkv, hq, d, seed = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import attention as oatt
     from oracle import pool as opool
-    rng = np.random.default_rng(seed)
-    bits = tagged_bits(1, ctx, seed_offset=seed)[0]
-    k = (rng.standard_normal((1, ctx, hkv, d), dtype=np.float32)
-         * np.exp(rng.uniform(np.log(0.5), np.log(4.0), (hkv, d))).astype(np.float32))
-    v = rng.standard_normal((1, ctx, hkv, d), dtype=np.float32)
-    q = rng.standard_normal((hq, d), dtype=np.float32)
-    n2 = int((bits == 2).sum()) // 32 * 32
-    cfg = opool.Config(total_slots=ctx + 32, offset=n2, n_layers=1, n_kv_heads=hkv, head_dim=d)
-    op = opool.OraclePool(cfg)
-    op.alloc("r", bits)
-    op.write_prefill("r", k, v)
-    op.partition("r")
+    key = (ctx, hkv, d, seed)
+    if key not in _CPU_CACHE:
+        rng = np.random.default_rng(seed)
+        bits = tagged_bits(1, ctx, seed_offset=seed)[0]
+        k = (rng.standard_normal((1, ctx, hkv, d), dtype=np.float32)
+             * np.exp(rng.uniform(np.log(0.5), np.log(4.0), (hkv, d))).astype(np.float32))
+        v = rng.standard_normal((1, ctx, hkv, d), dtype=np.float32)
+        n2 = int((bits == 2).sum()) // 32 * 32
+        op = opool.OraclePool(opool.Config(total_slots=ctx + 32, offset=n2, n_layers=1, n_kv_heads=hkv, head_dim=d))
+        op.alloc("r", bits)
+        op.write_prefill("r", k, v)
+        op.partition("r")
+        _CPU_CACHE[key] = op
+    op = _CPU_CACHE[key]
+    q = np.random.default_rng(seed + 1).standard_normal((hq, d), dtype=np.float32)
     t0 = time.perf_counter()
     oatt.flash_decode_pool(q, op, "r", 0)
     return time.perf_counter() - t0
 
 
-def cpu_baseline(args, n_units: int, workers: int) -> dict:
-    ctx_cpu = args.ctx
-    jobs = [(ctx_cpu, args.kv_heads, args.q_heads, args.head_dim, 1000 + i) for i in range(n_units)]
+def _init_worker():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["MKL_NUM_THREADS"] = "1"
+
+
+def cpu_baseline(args, n_units: int, workers: int, samples: int = 1, warmup: int = 0) -> dict:
+    """Oracle port of attention.py:175-218 on all host cores: ``workers`` processes time
+    independent (request, layer) units at full context; one sample = one unit per worker."""
+    jobs = [(args.ctx, args.kv_heads, args.q_heads, args.head_dim, 1000 + i) for i in range(n_units)]
     ctx_mp = mp.get_context("spawn")
     t0 = time.perf_counter()
-    with ctx_mp.Pool(workers) as p:
-        times = p.map(_cpu_unit, jobs)
+    with ctx_mp.Pool(workers, initializer=_init_worker) as p:
+        for _ in range(warmup):
+            p.map(_cpu_unit, jobs)
+        times = [t for _ in range(samples) for t in p.map(_cpu_unit, jobs)]
     wall = time.perf_counter() - t0
     per_unit = float(np.mean(times))
     units_per_step = args.batch * args.layers
-    # all cores busy on independent (request, layer) units
-    step_s = per_unit * units_per_step / workers
+    step_s = per_unit * units_per_step / workers  # all cores busy on independent units
     return {
         "value": args.batch / step_s,
         "unit": UNIT,
         "cores": workers,
         "kind": "port",
-        "sample": (f"{n_units} (request, layer) flash_decode units at {ctx_cpu} tokens, "
-                   f"{args.q_heads}/{args.kv_heads} heads, d={args.head_dim} (oracle restatement of "
-                   f"attention.py:175-218); mean {per_unit:.3f} s/unit, extrapolated to "
-                   f"{units_per_step} units/step over {workers} workers; sample wall {wall:.1f} s"),
+        "sample": (f"{len(times)} timed (request, layer) flash_decode units at {args.ctx} tokens, "
+                   f"{args.q_heads}/{args.kv_heads} heads, d={args.head_dim}, reference-tagged bits (oracle "
+                   f"restatement of attention.py:175-218, numpy fp32, 1 thread/process); mean {per_unit:.3f} "
+                   f"s/unit, extrapolated to {units_per_step} units/step over {workers} processes; "
+                   f"sample wall {wall:.1f} s incl. untimed oracle-pool builds"),
     }
 
 
 def run_reference(args):
+    """Reference arm: the reference's CPU path (oracle port; the reference is Python and
+    is not installable on the GPU box) on all host cores, same metric/config as ours."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     workers = os.cpu_count() or 1
-    n_units = max(workers, args.cpu_sample_units or workers)
-    per_step = []
-    res = None
-    for _ in range(max(1, args.steps if args.steps <= 2 else 1)):
-        res = cpu_baseline(args, n_units, workers)
-        per_step.append(res["value"])
+    res = cpu_baseline(args, workers, workers, samples=max(1, min(args.steps, 5)), warmup=0)
     value = res["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.batch / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference-tagged per-token bits, random K/V)",
-        "config": {"workload": "cfg2 decode attention: 64L, 64q/8kv heads, d128, batch 16, 32K ctx",
+        "config": {"workload": "cfg2 decode attention: 64 layers, 64q/8kv heads, d=128, batch 16, 32K ctx",
                    "batch": args.batch, "ctx": args.ctx, "layers": args.layers},
         "cpu_baseline": {"kind": res["kind"], "cores": res["cores"], "sample": res["sample"], "value": value,
                          "unit": UNIT},
