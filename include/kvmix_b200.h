@@ -8,11 +8,13 @@
  * interface it replaces -- see INTEGRATION.md for the ctypes binding.
  *
  * Device pool layout, G = 32, d = head_dim:
- *   int2_pool : uint8 [L][Hkv][n_pages][page_stride(d)]
- *               record = KeyPageBlock (d*G/4 + 4d B) || G INT2 V TokenBlocks (d/4 + 4d/G B each)
+ *   int2_pool : uint8 [L][Hkv][n_pages][page_stride(d) = 24 d]
+ *               record = KeyPageBlock (d*G/4 + 4d B) + G INT2 V TokenBlocks (d/4 + 4d/G B each)
  *   int4_pool : uint8 [L][Hkv][n_int4][slot_stride(d)]
- *               record = INT4 K TokenBlock (d/2 + 4d/G B) || INT4 V TokenBlock
- * Each block is the reference payload byte-for-byte (LAYOUT.md); strides round up to 16 B.
+ *               record = INT4 K TokenBlock (d/2 + 4d/G B) + INT4 V TokenBlock, padded to 16 B
+ * Every payload byte of every block (LAYOUT.md) is stored unmodified; inside a record the
+ * bytes are permuted so each decode lane loads its MMA fragment with one wide load
+ * (kvmix_page_layout / kvmix_slot_layout export the permutation).
  * Slot s < offset is INT2 page s/G row s%G; slot s >= offset is INT4 index s - offset.
  */
 #ifndef KVMIX_B200_H
@@ -42,6 +44,11 @@ const char* kvmix_last_error(void);
 /* record strides of the device pools (bytes) */
 int64_t kvmix_page_stride(int64_t head_dim);
 int64_t kvmix_slot_stride(int64_t head_dim);
+/* Host-only (no GPU needed): perm[i] = byte of the reference-order record (KeyPageBlock ||
+ * G INT2 V TokenBlocks, resp. INT4 K TokenBlock || INT4 V TokenBlock) stored at record byte i,
+ * -1 for padding.  perm has page_stride(d) / slot_stride(d) entries. */
+int kvmix_page_layout(int64_t head_dim, int64_t* perm);
+int kvmix_slot_layout(int64_t head_dim, int64_t* perm);
 /* payload sizes; replace quant.py:123-128 key_page_payload_bytes / token_block_payload_bytes */
 int64_t kvmix_key_page_payload_bytes(int64_t head_dim);
 int64_t kvmix_token_block_payload_bytes(int64_t head_dim, int64_t bitwidth);

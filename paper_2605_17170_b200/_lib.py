@@ -34,6 +34,8 @@ _SIGS = {
     "kvmix_last_error": ([], ctypes.c_char_p),
     "kvmix_page_stride": ([_I64], _I64),
     "kvmix_slot_stride": ([_I64], _I64),
+    "kvmix_page_layout": ([_I64, _P], ctypes.c_int),
+    "kvmix_slot_layout": ([_I64, _P], ctypes.c_int),
     "kvmix_key_page_payload_bytes": ([_I64], _I64),
     "kvmix_token_block_payload_bytes": ([_I64, _I64], _I64),
     "kvmix_encode_key_pages": ([_P, _I64, _I64, _P, _I64, _P, _P], ctypes.c_int),

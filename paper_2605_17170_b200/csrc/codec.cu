@@ -11,9 +11,11 @@ namespace kvmix {
 // ---------------------------------------------------------------------------------
 // One warp encodes one token vector x[0..D) as a TokenBlock (quant.py:189-232):
 // lane owns channels [lane*CPL, lane*CPL+CPL); groups of 32 channels are reduced
-// with segmented shuffles; codes are OR-reduced into 32-bit words.
-template <int D, int BITS>
-__device__ __forceinline__ void encode_token_warp(const float (&v)[D / 32], uint8_t* out, int lane, int32_t* err) {
+// with segmented shuffles; codes are OR-reduced into 32-bit words.  `st` places the
+// payload: st.code(word_index, word) gets code bytes [4w, 4w+4), st.param(j, s, z)
+// the fp16 bits of group j's (scale, zero).
+template <int D, int BITS, typename Store>
+__device__ __forceinline__ void encode_token_warp(const float (&v)[D / 32], const Store& st, int lane, int32_t* err) {
   constexpr int CPL = D / 32;               // channels per lane
   constexpr int LPG = 32 / CPL;             // lanes per group of 32 channels
   constexpr int LPW = 32 / (BITS * CPL);    // lanes per 32-bit code word
@@ -40,15 +42,15 @@ __device__ __forceinline__ void encode_token_warp(const float (&v)[D / 32], uint
   uint32_t word = bits << (BITS * CPL * (lane % LPW));
 #pragma unroll
   for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
-  if (lane % LPW == 0) reinterpret_cast<uint32_t*>(out)[lane / LPW] = word;
-  if (lane % LPG == 0)
-    reinterpret_cast<uint32_t*>(out + tok_code_bytes(D, BITS))[lane / LPG] = pack_param(scale, zero);
+  if (lane % LPW == 0) st.code(lane / LPW, word);
+  if (lane % LPG == 0) st.param(lane / LPG, pack_param(scale, zero));
 }
 
-// Thread c of a block encodes channel c of one KeyPageBlock (quant.py:160-177):
-// 32 token values of one channel -> 8 code bytes at [8c, 8c+8) + (scale, zero) at 8d+4c.
+// Thread c of a block encodes channel c of one KeyPageBlock (quant.py:160-177): 32
+// token values of one channel -> code bytes tau = 0..7 (tokens 4tau..4tau+3) stored in
+// KC row tau, (scale, zero) into KS / KZ (device record layout, common.cuh).
 template <int D>
-__device__ __forceinline__ void encode_key_channel(const float (&x)[G], uint8_t* out, int c, int32_t* err) {
+__device__ __forceinline__ void encode_key_channel(const float (&x)[G], uint8_t* rec, int c, int32_t* err) {
   float mn = x[0], mx = x[0];
   bool finite = true;
 #pragma unroll
@@ -66,9 +68,43 @@ __device__ __forceinline__ void encode_key_channel(const float (&x)[G], uint8_t*
     w0 |= quant_code(x[j], scale, zero, 3) << (2 * j);
     w1 |= quant_code(x[j + 16], scale, zero, 3) << (2 * j);
   }
-  reinterpret_cast<uint2*>(out)[c] = make_uint2(w0, w1);
-  reinterpret_cast<uint32_t*>(out + 8 * D)[c] = pack_param(scale, zero);
+#pragma unroll
+  for (int tau = 0; tau < 8; ++tau) rec[pg_kc_off(D, tau, c)] = (uint8_t)(((tau < 4 ? w0 : w1) >> (8 * (tau & 3))) & 0xffu);
+  const uint32_t pz = pack_param(scale, zero);
+  reinterpret_cast<uint16_t*>(rec + PG_KS(D))[pg_kp_idx(c)] = (uint16_t)(pz & 0xffffu);
+  reinterpret_cast<uint16_t*>(rec + PG_KZ(D))[pg_kp_idx(c)] = (uint16_t)(pz >> 16);
 }
+
+// TokenBlock placement inside a staged INT2 page record (token row t of the page).
+template <int D>
+struct PageVStore {
+  uint8_t* rec;
+  int t;
+  __device__ void code(int w, uint32_t word) const {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rec[PG_VC(D) + pg_vc_off(D, t, 4 * w + k)] = (uint8_t)(word >> (8 * k));
+  }
+  __device__ void param(int j, uint32_t pz) const {
+    reinterpret_cast<uint16_t*>(rec + PG_VS(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + PG_VZ(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz >> 16);
+  }
+};
+// INT4 TokenBlock placement inside a staged slot record: K (V = false) or V half.
+template <int D, bool V>
+struct SlotStore {
+  uint8_t* rec;
+  __device__ void code(int w, uint32_t word) const {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = 4 * w + k;
+      rec[V ? SL_VC(D) + sl_vc_off(D, i) : sl_kc_off(D, i)] = (uint8_t)(word >> (8 * k));
+    }
+  }
+  __device__ void param(int j, uint32_t pz) const {
+    reinterpret_cast<uint16_t*>(rec + (V ? SL_VS(D) : SL_KS(D)))[j] = (uint16_t)(pz & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + (V ? SL_VZ(D) : SL_KZ(D)))[j] = (uint16_t)(pz >> 16);
+  }
+};
 
 // ------------------------------ generic codec ----------------------------------------
 // Runtime head_dim (any d for key pages -- LAYOUT.md's worked example has d = 2 --,
@@ -225,7 +261,8 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t 
 // ------------------------------ pool data plane ----------------------------------------
 // write_prefill INT2 branch (pool.py:236-252 -> write_page :201-215): one block per
 // (request page, kv head, layer).  Threads c < D encode the KeyPageBlock column c;
-// the 4 warps encode the page's 32 INT2 V TokenBlocks in slot order.
+// the 4 warps encode the page's 32 INT2 V TokenBlocks.  The record is assembled in
+// shared memory in the device layout and leaves with coalesced 16-byte stores.
 template <int D, typename T>
 __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                             int64_t n_tokens, int64_t n_kv_heads,
@@ -235,6 +272,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
                                                             int32_t* err) {
   const int p = blockIdx.x, h = blockIdx.y, l = blockIdx.z;
   __shared__ int tok[G];
+  __shared__ __align__(16) uint8_t srec[page_stride(D)];
   if (threadIdx.x < G) tok[threadIdx.x] = page_tokens[(int64_t)p * G + threadIdx.x];
   __syncthreads();
   const int64_t page = page_ids[p];
@@ -244,20 +282,24 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     float x[G];
 #pragma unroll
     for (int j = 0; j < G; ++j) x[j] = to_f32(keys[elem(tok[j], c)]);
-    encode_key_channel<D>(x, rec, c, err);
+    encode_key_channel<D>(x, srec, c, err);
   }
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int j = warp; j < G; j += 4) {
     float v[D / 32];
 #pragma unroll
     for (int i = 0; i < D / 32; ++i) v[i] = to_f32(values[elem(tok[j], lane * (D / 32) + i)]);
-    encode_token_warp<D, 2>(v, rec + key_page_bytes(D) + j * tok_bytes(D, 2), lane, err);
+    encode_token_warp<D, 2>(v, PageVStore<D>{srec, j}, lane, err);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < page_stride(D) / 16; i += 128)
+    reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
 }
 
 // INT4 tokens: write_prefill :253-262, write_token :217-226, append_decode_token :284-306.
 // Warp per (token, kv head, layer); input element (l, t, h, c) at
-// ((t_stride_l * l) + t * tok_stride + h * D + c) with explicit strides.
+// ((t_stride_l * l) + t * tok_stride + h * D + c) with explicit strides.  The slot
+// record is staged per warp in shared memory (device layout) and stored as 16 B words.
 template <int D, typename T>
 __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                           int64_t n, int64_t layer_stride, int64_t tok_stride,
@@ -266,21 +308,28 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
                                                           const int32_t* __restrict__ int4_ids,
                                                           uint8_t* __restrict__ int4_pool, int64_t pool_int4,
                                                           int32_t* err) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (int64_t)blockIdx.x * 4 + threadIdx.x / 32;
+  constexpr int SS = slot_stride(D);
+  __shared__ __align__(16) uint8_t srec[4][SS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x / 32;
+  const int64_t i = (int64_t)blockIdx.x * 4 + warp;
   const int h = blockIdx.y, l = blockIdx.z;
   if (i >= n) return;
+  uint8_t* st = srec[warp];
+  for (int k = lane; k < SS / 4; k += 32) reinterpret_cast<uint32_t*>(st)[k] = 0u;  // padding stays zero
+  __syncwarp();
   const int64_t t = tokens ? tokens[i] : i;
   const int64_t base = l * layer_stride + t * tok_stride + (int64_t)h * D + lane * (D / 32);
   uint8_t* rec =
-      int4_pool + (((layer0 + l) * n_kv_heads + h) * pool_int4 + (int64_t)int4_ids[i]) * slot_stride(D);
+      int4_pool + (((layer0 + l) * n_kv_heads + h) * pool_int4 + (int64_t)int4_ids[i]) * SS;
   float v[D / 32];
 #pragma unroll
   for (int k = 0; k < D / 32; ++k) v[k] = to_f32(keys[base + k]);
-  encode_token_warp<D, 4>(v, rec, lane, err);
+  encode_token_warp<D, 4>(v, SlotStore<D, false>{st}, lane, err);
 #pragma unroll
   for (int k = 0; k < D / 32; ++k) v[k] = to_f32(values[base + k]);
-  encode_token_warp<D, 4>(v, rec + tok_bytes(D, 4), lane, err);
+  encode_token_warp<D, 4>(v, SlotStore<D, true>{st}, lane, err);
+  __syncwarp();
+  if (lane < SS / 16) reinterpret_cast<uint4*>(rec)[lane] = reinterpret_cast<const uint4*>(st)[lane];
 }
 
 // K5 gather-dequant (pool.py:394-439): thread per (slot, head, channel) -> f32 k/v.
@@ -295,24 +344,26 @@ __global__ void gather_dequant_kernel(const uint8_t* __restrict__ int2_pool, con
   const int64_t h = (idx / D) % n_kv_heads;
   const int64_t i = idx / (D * n_kv_heads);
   const int64_t slot = slots[i];
-  auto deq = [](const uint8_t* blk, int c, int bits) {
-    uint32_t code = (blk[c * bits / 8] >> ((c * bits) & 7)) & ((1u << bits) - 1);
-    const __half2 pz = *reinterpret_cast<const __half2*>(blk + D * bits / 8 + 4 * (c / G));
-    return __fmaf_rn((float)code, __low2float(pz), __high2float(pz));
+  auto half_at = [](const uint8_t* p, int idx) {
+    return __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(p)[idx]));
   };
   float kv, vv;
   if (slot < offset) {
     const int64_t page = slot / G;
     const int row = (int)(slot % G);
     const uint8_t* rec = int2_pool + ((layer * n_kv_heads + h) * pool_pages + page) * page_stride(D);
-    uint32_t code = (rec[8 * c + row / 4] >> (2 * (row & 3))) & 3u;
-    const __half2 pz = *reinterpret_cast<const __half2*>(rec + 8 * D + 4 * c);
-    kv = __fmaf_rn((float)code, __low2float(pz), __high2float(pz));
-    vv = deq(rec + key_page_bytes(D) + row * tok_bytes(D, 2), c, 2);
+    const uint32_t kc = (rec[pg_kc_off(D, row >> 2, c)] >> (2 * (row & 3))) & 3u;
+    kv = __fmaf_rn((float)kc, half_at(rec + PG_KS(D), pg_kp_idx(c)), half_at(rec + PG_KZ(D), pg_kp_idx(c)));
+    const uint32_t vc = (rec[PG_VC(D) + pg_vc_off(D, row, c >> 2)] >> (2 * (c & 3))) & 3u;
+    const int pj = pg_vp_idx(D, row, c / G);
+    vv = __fmaf_rn((float)vc, half_at(rec + PG_VS(D), pj), half_at(rec + PG_VZ(D), pj));
   } else {
     const uint8_t* rec = int4_pool + ((layer * n_kv_heads + h) * pool_int4 + (slot - offset)) * slot_stride(D);
-    kv = deq(rec, c, 4);
-    vv = deq(rec + tok_bytes(D, 4), c, 4);
+    const int sh = 4 * (c & 1);
+    const uint32_t kc = (rec[sl_kc_off(D, c >> 1)] >> sh) & 15u;
+    kv = __fmaf_rn((float)kc, half_at(rec + SL_KS(D), c / G), half_at(rec + SL_KZ(D), c / G));
+    const uint32_t vc = (rec[SL_VC(D) + sl_vc_off(D, c >> 1)] >> sh) & 15u;
+    vv = __fmaf_rn((float)vc, half_at(rec + SL_VS(D), c / G), half_at(rec + SL_VZ(D), c / G));
   }
   k_out[idx] = kv;
   v_out[idx] = vv;
@@ -334,6 +385,47 @@ using namespace kvmix;
 
 extern "C" int64_t kvmix_page_stride(int64_t d) { return page_stride((int)d); }
 extern "C" int64_t kvmix_slot_stride(int64_t d) { return slot_stride((int)d); }
+// Host-side export of the record permutation the kernels use (same constexpr helpers).
+extern "C" int kvmix_page_layout(int64_t d, int64_t* perm) {
+  if (d < 32 || d > 256 || d % 32) return fail(KVMIX_EINVAL, "head_dim must be 32, 64, 128 or 256");
+  const int D = (int)d, ng = D / 32, kp = key_page_bytes(D), tb2 = tok_bytes(D, 2);
+  for (int i = 0; i < page_stride(D); ++i) perm[i] = -1;
+  for (int c = 0; c < D; ++c) {
+    for (int tau = 0; tau < 8; ++tau) perm[pg_kc_off(D, tau, c)] = 8 * c + tau;
+    for (int k = 0; k < 2; ++k) {
+      perm[PG_KS(D) + 2 * pg_kp_idx(c) + k] = 8 * D + 4 * c + k;
+      perm[PG_KZ(D) + 2 * pg_kp_idx(c) + k] = 8 * D + 4 * c + 2 + k;
+    }
+  }
+  for (int t = 0; t < G; ++t) {
+    for (int b = 0; b < D / 4; ++b) perm[PG_VC(D) + pg_vc_off(D, t, b)] = kp + t * tb2 + b;
+    for (int j = 0; j < ng; ++j)
+      for (int k = 0; k < 2; ++k) {
+        perm[PG_VS(D) + 2 * pg_vp_idx(D, t, j) + k] = kp + t * tb2 + D / 4 + 4 * j + k;
+        perm[PG_VZ(D) + 2 * pg_vp_idx(D, t, j) + k] = kp + t * tb2 + D / 4 + 4 * j + 2 + k;
+      }
+  }
+  return KVMIX_OK;
+}
+
+extern "C" int kvmix_slot_layout(int64_t d, int64_t* perm) {
+  if (d < 32 || d > 256 || d % 32) return fail(KVMIX_EINVAL, "head_dim must be 32, 64, 128 or 256");
+  const int D = (int)d, ng = D / 32, tb4 = tok_bytes(D, 4);
+  for (int i = 0; i < slot_stride(D); ++i) perm[i] = -1;
+  for (int i = 0; i < D / 2; ++i) {
+    perm[sl_kc_off(D, i)] = i;
+    perm[SL_VC(D) + sl_vc_off(D, i)] = tb4 + i;
+  }
+  for (int j = 0; j < ng; ++j)
+    for (int k = 0; k < 2; ++k) {
+      perm[SL_KS(D) + 2 * j + k] = D / 2 + 4 * j + k;
+      perm[SL_KZ(D) + 2 * j + k] = D / 2 + 4 * j + 2 + k;
+      perm[SL_VS(D) + 2 * j + k] = tb4 + D / 2 + 4 * j + k;
+      perm[SL_VZ(D) + 2 * j + k] = tb4 + D / 2 + 4 * j + 2 + k;
+    }
+  return KVMIX_OK;
+}
+
 extern "C" int64_t kvmix_key_page_payload_bytes(int64_t d) { return key_page_bytes((int)d); }
 extern "C" int64_t kvmix_token_block_payload_bytes(int64_t d, int64_t b) { return tok_bytes((int)d, (int)b); }
 

@@ -34,7 +34,6 @@ namespace kvmix {
 #endif
 constexpr int NW = 4;                 // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
-constexpr uint32_t MAGIC = 0x3C003C00u;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_SLACK = 8.f;  // see softmax_tile
 
@@ -73,25 +72,6 @@ __device__ __forceinline__ float load_q(const DecodeArgs& a, int64_t idx) {
   if (a.q_dtype == KVMIX_F32) return reinterpret_cast<const float*>(a.q)[idx];
   if (a.q_dtype == KVMIX_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.q)[idx]);
   return __half2float(reinterpret_cast<const __half*>(a.q)[idx]);
-}
-
-template <int NG>
-__device__ __forceinline__ void lds_params(const uint8_t* p, uint32_t (&w)[NG]) {
-  if constexpr (NG == 4) {
-    uint4 v = *reinterpret_cast<const uint4*>(p);
-    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-  } else if constexpr (NG == 2) {
-    uint2 v = *reinterpret_cast<const uint2*>(p);
-    w[0] = v.x; w[1] = v.y;
-  } else {
-    w[0] = *reinterpret_cast<const uint32_t*>(p);
-  }
-}
-__device__ __forceinline__ uint32_t lds32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
-
-// code * 2^(2e-10) for the 2-bit field e of each half (INT2 codes in bits 2e..2e+1)
-__device__ __forceinline__ uint32_t int2_field(uint32_t r, int e) {
-  return hsub2u(lop_and_or(r, 0x00030003u << (2 * e), MAGIC), MAGIC);
 }
 
 // ------------------------------------------------------------------------------------
@@ -237,207 +217,225 @@ __device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, 
   bP[1][1] = movtrans(pack_h2(p[6], p[7]));
 }
 
-// PV for one k-step and one channel group j: A = code fields of the pair-A / pair-B
-// tokens (rows e = 0..3 -> channels 32j + 4g + e), B = P' = p*s.
-template <int D>
-__device__ __forceinline__ void pv_group(Acc<D>& acc, int j, const uint32_t (&fA)[4], const uint32_t (&fB)[4],
-                                         uint32_t bP0, uint32_t bP1, uint32_t pA0, uint32_t pA1, uint32_t pB0,
-                                         uint32_t pB1) {
-  const uint64_t ps = pack_b64(hmul2u(bP0, prmt(pA0, pA1, 0x5410)), hmul2u(bP1, prmt(pB0, pB1, 0x5410)));
-  mma16816_b64(acc.o[2 * j], fA[0], fA[1], fB[0], fB[1], ps);
-  mma16816_b64(acc.o[2 * j + 1], fA[2], fA[3], fB[2], fB[3], ps);
+// Shared-memory vector load of NB bytes (2, 4, 8, 16 or a multiple of 16) into words.
+template <int NB>
+__device__ __forceinline__ void lds_vec(const uint8_t* p, uint32_t* w) {
+  if constexpr (NB >= 16) {
+#pragma unroll
+    for (int i = 0; i < NB / 16; ++i) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[i];
+      w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+    }
+  } else if constexpr (NB == 8) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    w[0] = v.x; w[1] = v.y;
+  } else if constexpr (NB == 4) {
+    w[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else {
+    w[0] = *reinterpret_cast<const uint16_t*>(p);
+  }
+}
+// low / high fp16 of x and of y as one half2 (low = x's half, high = y's half)
+__device__ __forceinline__ uint32_t pair_h(uint32_t x, uint32_t y, int hi) { return prmt(x, y, hi ? 0x7632u : 0x5410u); }
+__device__ __forceinline__ float half_f(uint32_t w, int hi) {
+  return __half2float(__ushort_as_half((unsigned short)(hi ? w >> 16 : w & 0xffffu)));
 }
 
-// sum_t p_th z_tj for all groups j at once: A = Z^T (row g = group g&3, k = PV tokens),
-// B = P^T.  zA0..zB1 are the (scale, zero) words of group g&3 of the 4 tokens.
-template <int D>
-__device__ __forceinline__ void pv_zeros(Acc<D>& acc, uint32_t zA0, uint32_t zA1, uint32_t zB0, uint32_t zB1,
-                                         uint32_t bP0, uint32_t bP1) {
-  const uint32_t zA = prmt(zA0, zA1, 0x7632), zB = prmt(zB0, zB1, 0x7632);
-  // rows g+8 (a1, a3) are don't-care: feed the raw words to avoid register moves
-  mma16816_b64(acc.zs, zA, zA0, zB, zB0, pack_b64(bP0, bP1));
-}
+// Codes enter the MMA as fp16 SUBNORMALS: a 2-bit field masked into mantissa bits 4-5
+// is code * 2^-20, bits 6-7 code * 2^-18 (INT4 nibbles: bits 4-7 -> 2^-20, 6-9 -> 2^-18).
+// One LOP3 per two codes, no magic-number subtraction; the power of two is undone in
+// fp32 per row.  Mantissa bits >= 4 keep the tensor core's subnormal products within
+// ~5e-6 of exact (measured, tools/microbench/denorm.cu); bits 0-3 would not.
+constexpr uint32_t M2A = 0x00300030u, M2B = 0x00C000C0u;  // INT2 field at bits 4-5 / 6-7
+constexpr uint32_t M4A = 0x00F000F0u, M4B = 0x03C003C0u;  // INT4 nibble at bits 4-7 / 6-9
+constexpr float P20 = 1048576.f, P18 = 262144.f;
 
-// Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).  b2: INT2 key
-// pages, chunk i, lane q pairs channels (16i+4q+{0,1}) / (16i+4q+{2,3}); b4: INT4 keys,
-// chunk 2j+s pairs (32j+8q+{0,4}) / ({1,5}) (s=0) or ({2,6}) / ({3,7}) (s=1).  With LO
-// (fp32 q), *lo hold q - fp16(q) so the bias and INT4 products see ~22-bit q.
+// Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).
+//  b2[I]  INT2 key pages, chunk I, lane q: channels cb = q*D/4 + 4I: (cb, cb+2) / (cb+1, cb+3)
+//  b4[2j], b4[2j+1]  INT4 keys, group j, lane q: cb = 32j + 8q: (cb+1, cb+5) / (cb, cb+4) and
+//         (cb+2, cb+6) / (cb+3, cb+7)
+//  qz     (Q_2q, Q_2q+1) / 0 with Q_j = sum of q over channel group j (hi and lo fp16 parts)
+// With LO (fp32 q) the *lo arrays hold q - fp16(q).
 template <int D, bool LO>
 struct QFrag {
   uint64_t b2[D / 16], b4[D / 16];
   uint64_t b2lo[LO ? D / 16 : 1], b4lo[LO ? D / 16 : 1];
+  uint64_t qz, qzlo;
 };
 
 // ---------------------------------- INT2 page tile ----------------------------------
+// Record layout: common.cuh PG_* (layout.py).  QK rows: M tile 0 rows g / g+8 = tokens
+// 4g / 4g+1 (fields 0 / 1), M tile 1 = tokens 4g+2 / 4g+3.  PV k-step ks, lane q covers
+// tokens T0 = 8q + 2ks, T1 = T0 + 4 (a0) and T0+1, T1+1 (a2).
 template <int D, bool LO>
 __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
                                           int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
+  constexpr int KB = D / 4, NG = C::NGRP, LB = KB < 16 ? KB : 16;
   const int g = lane >> 2, q = lane & 3;
-  // lane g reads byte beta(g) = (g>>1) | ((g&1)<<2) of every channel word -> tokens 4beta..4beta+3
-  // chunk i, lane q: k pair (2q, 2q+1) = channels 16i+4q+{0,1}, (2q+8, 2q+9) = 16i+4q+{2,3}
-  const uint32_t selK = (uint32_t)(g >> 1) | ((uint32_t)(4 + (g >> 1)) << 8);
-  const uint8_t* kb = buf + 32 * q + 4 * (g & 1);  // channel word 16i+4q+e: + 128 i + 8 e
-  const uint8_t* pb = buf + 8 * D + 16 * q;         // (s, z) of channels 16i+4q+{0..3}: + 64 i
+  uint32_t kw[C::NCH], ksw[2 * C::NCH], kzw[2 * C::NCH];
+#pragma unroll
+  for (int o = 0; o < KB; o += LB) {
+    const int p = q * KB + o;
+    lds_vec<LB>(buf + g * D + ((((p >> 4) ^ (g & 1)) << 4) | (p & 15)), kw + o / 4);
+  }
+  lds_vec<2 * KB>(buf + PG_KS(D) + 2 * q * KB, ksw);
+  lds_vec<2 * KB>(buf + PG_KZ(D) + 2 * q * KB, kzw);
   float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < C::NCH; ++i) {
-    const uint32_t r1 = prmt(ld_s32(kb, 128 * i), ld_s32(kb, 128 * i + 8), selK);
-    const uint32_t r2 = prmt(ld_s32(kb, 128 * i + 16), ld_s32(kb, 128 * i + 24), selK);
-    const uint4 pv = *reinterpret_cast<const uint4*>(pb + 64 * i);
+    const uint32_t w = kw[i], u = w << 4, v = w >> 4, x = w >> 8;
     const uint64_t qi = qf.b2[i];
-    const uint64_t qs = pack_b64(hmul2u(lo32(qi), prmt(pv.x, pv.y, 0x5410)), hmul2u(hi32(qi), prmt(pv.z, pv.w, 0x5410)));
-    const uint32_t z1 = prmt(pv.x, pv.y, 0x7632), z2 = prmt(pv.z, pv.w, 0x7632);
-    mma16816_b64(c0, int2_field(r1, 0), int2_field(r1, 1), int2_field(r2, 0), int2_field(r2, 1), qs);
-    mma16816_b64(c1, int2_field(r1, 2), int2_field(r1, 3), int2_field(r2, 2), int2_field(r2, 3), qs);
+    const uint64_t qs = pack_b64(hmul2u(lo32(qi), ksw[2 * i]), hmul2u(hi32(qi), ksw[2 * i + 1]));
+    mma16816_b64(c0, u & M2A, u & M2B, v & M2A, v & M2B, qs);
+    mma16816_b64(c1, w & M2A, w & M2B, x & M2A, x & M2B, qs);
     // bias rows g carry sum_c q_c z_c; rows g+8 (cb[2], cb[3]) are don't-care filler
-    mma16816_b64(cb, z1, r1, z2, r2, qi);
-    if constexpr (LO) mma16816_b64(cb, z1, r1, z2, r2, qf.b2lo[i]);
+    mma16816_b64(cb, kzw[2 * i], kzw[2 * i], kzw[2 * i + 1], kzw[2 * i + 1], qi);
+    if constexpr (LO) mma16816_b64(cb, kzw[2 * i], kzw[2 * i], kzw[2 * i + 1], kzw[2 * i + 1], qf.b2lo[i]);
   }
-  // undo 2^(2k-10) per token row (k = token position inside its code byte), apply scale*log2(e)
   const float b0 = cb[0] * qscale, b1 = cb[1] * qscale;
-  const float sv[8] = {fmaf(c0[0], 1024.f * qscale, b0), fmaf(c0[1], 1024.f * qscale, b1),
-                       fmaf(c0[2], 256.f * qscale, b0),  fmaf(c0[3], 256.f * qscale, b1),
-                       fmaf(c1[0], 64.f * qscale, b0),   fmaf(c1[1], 64.f * qscale, b1),
-                       fmaf(c1[2], 16.f * qscale, b0),   fmaf(c1[3], 16.f * qscale, b1)};
+  const float fa = P20 * qscale, fb = P18 * qscale;
+  const float sv[8] = {fmaf(c0[0], fa, b0), fmaf(c0[1], fa, b1), fmaf(c0[2], fb, b0), fmaf(c0[3], fb, b1),
+                       fmaf(c1[0], fa, b0), fmaf(c1[1], fa, b1), fmaf(c1[2], fb, b0), fmaf(c1[3], fb, b1)};
   uint32_t bP[2][2];
   softmax_tile<D>(sv, st, acc, bP);
-  // PV: k-step ks, pair A tokens (4q+2ks, 16+4q+2ks), pair B = pair A + 1
-  const uint32_t selV = (uint32_t)(g & 3) | ((uint32_t)(4 + (g & 3)) << 8);
-  const uint8_t* vb = buf + C::KP + C::TB2 * 4 * q;  // token 4q's V block
-  const uint8_t* vc = vb + 4 * (g >> 2);             // + 8j: word of byte 8j+g
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
-    constexpr int T = C::TB2;
-    uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
-    lds_params<C::NGRP>(vb + (2 * ks) * T + D / 4, pA0);
-    lds_params<C::NGRP>(vb + (16 + 2 * ks) * T + D / 4, pA1);
-    lds_params<C::NGRP>(vb + (2 * ks + 1) * T + D / 4, pB0);
-    lds_params<C::NGRP>(vb + (17 + 2 * ks) * T + D / 4, pB1);
-    {
-      const uint8_t* zb = vb + D / 4 + 4 * (g & (C::NGRP - 1));
-      pv_zeros<D>(acc, ld_s32(zb, (2 * ks) * T), ld_s32(zb, (16 + 2 * ks) * T), ld_s32(zb, (2 * ks + 1) * T),
-                  ld_s32(zb, (17 + 2 * ks) * T), bP[ks][0], bP[ks][1]);
-    }
+    uint32_t vw[NG], vs[2 * NG], vz[2];
+    lds_vec<4 * NG>(buf + PG_VC(D) + ((ks * 8 + g) * 4 + q) * NG * 4, vw);
+    lds_vec<8 * NG>(buf + PG_VS(D) + (ks * 4 + q) * NG * 8, vs);
+    lds_vec<8>(buf + PG_VZ(D) + ((ks * 4 + q) * NG + (g & (NG - 1))) * 8, vz);
+    // sum_t p_th z_tj for all groups at once: A = Z^T (row g = group g & (NG-1)), B = P^T
+    mma16816_b64(acc.zs, vz[0], vz[0], vz[1], vz[1], pack_b64(bP[ks][0], bP[ks][1]));
 #pragma unroll
-    for (int j = 0; j < C::NGRP; ++j) {
-      const uint32_t rA = prmt(ld_s32(vc, (2 * ks) * T + 8 * j), ld_s32(vc, (16 + 2 * ks) * T + 8 * j), selV);
-      const uint32_t rB = prmt(ld_s32(vc, (2 * ks + 1) * T + 8 * j), ld_s32(vc, (17 + 2 * ks) * T + 8 * j), selV);
-      uint32_t fA[4], fB[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        fA[e] = int2_field(rA, e);
-        fB[e] = int2_field(rB, e);
-      }
-      pv_group<D>(acc, j, fA, fB, bP[ks][0], bP[ks][1], pA0[j], pA1[j], pB0[j], pB1[j]);
+    for (int j = 0; j < NG; ++j) {
+      const uint32_t w = vw[j], u = w << 4, v = w >> 4, x = w >> 8;
+      const uint64_t ps = pack_b64(hmul2u(bP[ks][0], vs[2 * j]), hmul2u(bP[ks][1], vs[2 * j + 1]));
+      mma16816_b64(acc.o[2 * j], u & M2A, u & M2B, v & M2A, v & M2B, ps);
+      mma16816_b64(acc.o[2 * j + 1], w & M2A, w & M2B, x & M2A, x & M2B, ps);
     }
   }
 }
 
 // ---------------------------------- INT4 slot tile ----------------------------------
-__device__ __forceinline__ uint32_t int4_deq(uint32_t field16, uint32_t s16, uint32_t zz) {
-  return hfma2u(hsub2u(field16, MAGIC), s16, zz);  // (code/16) * 16s + z
-}
+// Row -> slot map inside an M tile: rows 0-7 -> rho(r), rows 8-15 -> 8 + rho(r - 8) with
+// rho = [0,2,1,3,6,4,7,5]: QK K loads (lanes g = 2p, 2p+1 two slots apart) and PV V
+// loads (rho(2q) and rho(2q+1) each distinct mod 4) are both bank-conflict-free at the
+// 160 B slot stride.
+__device__ __forceinline__ int rho(int r) { return (0x57463120u >> (4 * r)) & 7; }
 
 template <int D, bool FULL, bool LO>
 __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const QFrag<D, LO>& qf,
                                           float qscale, int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
-  constexpr int S = C::SS;
+  constexpr int S = C::SS, NG = C::NGRP;
   const int g = lane >> 2, q = lane & 3;
-  // QK row g of M tile m is slot 16m + beta(g), row g+8 is slot 16m + 8 + beta(g), with
-  // beta(g) = (g>>1) | ((g&1)<<2): PV lanes then read 4 slots 1 apart (conflict-free V loads)
-  const int beta = (g >> 1) | ((g & 1) << 2);
-  const uint8_t* kb = buf + S * beta + 4 * q;  // slot row r: + S*(16(r>>1) + 8(r&1)); group j: + 16j
-  const uint8_t* kp = buf + S * beta + D / 2;  // K params of the slot: + 4j
-  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+  const float fs = P20 * qscale;
+  float sv[8];
 #pragma unroll
-  for (int j = 0; j < C::NGRP; ++j) {
-    uint32_t e[4][4];  // [slot row: M0 g, M0 g+8, M1 g, M1 g+8][field]
+  for (int mt = 0; mt < 2; ++mt) {
+    const int sa = 16 * mt + rho(g), sb = sa + 8;
+    uint32_t kwa[NG], kwb[NG], pa[NG], pb[NG];
+    lds_vec<4 * NG>(buf + S * sa + 4 * NG * q, kwa);
+    lds_vec<4 * NG>(buf + S * sb + 4 * NG * q, kwb);
+    lds_vec<4 * NG>(buf + S * sa + SL_KS(D), pa);  // NG scales then NG zeros
+    lds_vec<4 * NG>(buf + S * sb + SL_KS(D), pb);
+    // D_j = sum over group j of q_c code_c (per-token group scales are applied in fp32)
+    float dj[NG][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int ro = S * (16 * (r >> 1) + 8 * (r & 1));
-      const uint32_t w = ld_s32(kb, ro + 16 * j);
-      const uint32_t par = ld_s32(kp, ro + 4 * j);
-      const uint32_t s16 = hmul2u(prmt(par, par, 0x1010), 0x4C004C00u);  // (16s, 16s)
-      const uint32_t zz = prmt(par, par, 0x3232);
-      e[r][0] = int4_deq(lop_and_or(w << 6, 0x03C003C0u, MAGIC), s16, zz);
-      e[r][1] = int4_deq(lop_and_or(w << 2, 0x03C003C0u, MAGIC), s16, zz);
-      e[r][2] = int4_deq(lop_and_or(w >> 2, 0x03C003C0u, MAGIC), s16, zz);
-      e[r][3] = int4_deq(lop_and_or(w >> 6, 0x03C003C0u, MAGIC), s16, zz);
+    for (int j = 0; j < NG; ++j) {
+      dj[j][0] = dj[j][1] = dj[j][2] = dj[j][3] = 0.f;
+      const uint32_t wa = kwa[j], wb = kwb[j];
+      mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4[2 * j]);
+      mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4[2 * j + 1]);
+      if constexpr (LO) {
+        mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4lo[2 * j]);
+        mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4lo[2 * j + 1]);
+      }
     }
-    const uint64_t qa = qf.b4[2 * j], qc = qf.b4[2 * j + 1];
-    mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], qa);
-    mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], qc);
-    mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], qa);
-    mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], qc);
-    if constexpr (LO) {
-      const uint64_t la = qf.b4lo[2 * j], lc = qf.b4lo[2 * j + 1];
-      mma16816_b64(c0, e[0][0], e[1][0], e[0][1], e[1][1], la);
-      mma16816_b64(c0, e[0][2], e[1][2], e[0][3], e[1][3], lc);
-      mma16816_b64(c1, e[2][0], e[3][0], e[2][1], e[3][1], la);
-      mma16816_b64(c1, e[2][2], e[3][2], e[2][3], e[3][3], lc);
+    // sum_j z_j Q_j: A row = token, k = 2q, 2q+1 -> groups 2q, 2q+1 (lanes with 2q >= NG give 0)
+    uint32_t za = 0u, zb = 0u;
+    if constexpr (NG == 4) {
+      if (q < 2) { za = q ? pa[3] : pa[2]; zb = q ? pb[3] : pb[2]; }
+    } else if constexpr (NG == 2) {
+      if (q == 0) { za = pa[1]; zb = pb[1]; }
+    } else {
+      if (q == 0) { za = pa[0] >> 16; zb = pb[0] >> 16; }
     }
-  }
-  float sv[8] = {c0[0] * qscale, c0[1] * qscale, c0[2] * qscale, c0[3] * qscale,
-                 c1[0] * qscale, c1[1] * qscale, c1[2] * qscale, c1[3] * qscale};
-  if (!FULL) {
-    if (beta >= nv) sv[0] = sv[1] = -INFINITY;
-    if (beta + 8 >= nv) sv[2] = sv[3] = -INFINITY;
-    if (beta + 16 >= nv) sv[4] = sv[5] = -INFINITY;
-    if (beta + 24 >= nv) sv[6] = sv[7] = -INFINITY;
+    float zq[4] = {0.f, 0.f, 0.f, 0.f};
+    mma16816_b64(zq, za, zb, 0u, 0u, qf.qz);
+    mma16816_b64(zq, za, zb, 0u, 0u, qf.qzlo);
+    float ta0 = zq[0] * qscale, ta1 = zq[1] * qscale, tb0 = zq[2] * qscale, tb1 = zq[3] * qscale;
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      const float s_a = half_f(pa[j >> 1], j & 1) * fs, s_b = half_f(pb[j >> 1], j & 1) * fs;
+      ta0 = fmaf(s_a, dj[j][0], ta0);
+      ta1 = fmaf(s_a, dj[j][1], ta1);
+      tb0 = fmaf(s_b, dj[j][2], tb0);
+      tb1 = fmaf(s_b, dj[j][3], tb1);
+    }
+    if (!FULL) {
+      if (sa >= nv) ta0 = ta1 = -INFINITY;
+      if (sb >= nv) tb0 = tb1 = -INFINITY;
+    }
+    sv[4 * mt] = ta0;
+    sv[4 * mt + 1] = ta1;
+    sv[4 * mt + 2] = tb0;
+    sv[4 * mt + 3] = tb1;
   }
   uint32_t bP[2][2];
   softmax_tile<D>(sv, st, acc, bP);
-  const uint32_t b4 = 2 * (g & 1);
-  const uint32_t selV = b4 | ((b4 + 1) << 4) | ((b4 + 4) << 8) | ((b4 + 5) << 12);
-  // PV k-step ks: pair A = QK rows (2q, 2q+1) = slots 16ks + q, 16ks + q + 4; pair B = + 8
-  const uint8_t* vb = buf + S * q + C::TB4;  // slot q's V block
-  const uint8_t* vc = vb + 4 * (g >> 1);     // + 16j: word holding bytes 16j+2g, +1
+  // PV k-step ks: k = 2q, 2q+1, 2q+8, 2q+9 = rows of QK M tile ks -> slots ta, tb, tc, td
+  constexpr int VB = 2 * NG;  // this lane's code bytes per token: 2 per group
+  constexpr int VWN = VB < 4 ? 1 : VB / 4;
+  const int jz = g & (NG - 1);
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
-    uint32_t pA0[C::NGRP], pA1[C::NGRP], pB0[C::NGRP], pB1[C::NGRP];
-    lds_params<C::NGRP>(vb + S * (16 * ks) + D / 2, pA0);
-    lds_params<C::NGRP>(vb + S * (16 * ks + 4) + D / 2, pA1);
-    lds_params<C::NGRP>(vb + S * (16 * ks + 8) + D / 2, pB0);
-    lds_params<C::NGRP>(vb + S * (16 * ks + 12) + D / 2, pB1);
-    if (!FULL) {
-      const int sA0 = 16 * ks + q;
+    const int ta = 16 * ks + rho(2 * q), tb = 16 * ks + rho(2 * q + 1), tc = ta + 8, td = tb + 8;
+    uint32_t va[VWN], vb[VWN], vc[VWN], vd[VWN], pa[NG], pb[NG], pc[NG], pd[NG];
+    lds_vec<VB>(buf + S * ta + SL_VC(D) + VB * g, va);
+    lds_vec<VB>(buf + S * tb + SL_VC(D) + VB * g, vb);
+    lds_vec<VB>(buf + S * tc + SL_VC(D) + VB * g, vc);
+    lds_vec<VB>(buf + S * td + SL_VC(D) + VB * g, vd);
+    lds_vec<4 * NG>(buf + S * ta + SL_VS(D), pa);  // NG scales then NG zeros
+    lds_vec<4 * NG>(buf + S * tb + SL_VS(D), pb);
+    lds_vec<4 * NG>(buf + S * tc + SL_VS(D), pc);
+    lds_vec<4 * NG>(buf + S * td + SL_VS(D), pd);
+    if (!FULL) {  // padding slots: P = 0 already; zero their params so stale bytes cannot give NaN
 #pragma unroll
-      for (int j = 0; j < C::NGRP; ++j) {
-        if (sA0 >= nv) pA0[j] = 0u;
-        if (sA0 + 4 >= nv) pA1[j] = 0u;
-        if (sA0 + 8 >= nv) pB0[j] = 0u;
-        if (sA0 + 12 >= nv) pB1[j] = 0u;
+      for (int j = 0; j < NG; ++j) {
+        if (ta >= nv) pa[j] = 0u;
+        if (tb >= nv) pb[j] = 0u;
+        if (tc >= nv) pc[j] = 0u;
+        if (td >= nv) pd[j] = 0u;
       }
     }
+    // word / half holding the scale (Z = false) or zero (Z = true) of group j
+    auto pw = [&](const uint32_t* p, int j, bool z) -> uint32_t {  // j may be lane-dependent: select, never index
+      if constexpr (NG == 4) return z ? ((j >> 1) ? p[3] : p[2]) : ((j >> 1) ? p[1] : p[0]);
+      else if constexpr (NG == 2) return p[z ? 1 : 0];
+      else return p[0];
+    };
+    auto ph = [&](int j, bool z) -> int {
+      if constexpr (NG == 4) return j & 1;
+      else if constexpr (NG == 2) return j;
+      else return z ? 1 : 0;
+    };
     {
-      const uint8_t* zb = vb + D / 2 + 4 * (g & (C::NGRP - 1));
-      uint32_t zA0 = ld_s32(zb, S * (16 * ks)), zA1 = ld_s32(zb, S * (16 * ks + 4));
-      uint32_t zB0 = ld_s32(zb, S * (16 * ks + 8)), zB1 = ld_s32(zb, S * (16 * ks + 12));
-      if (!FULL) {
-        const int sA0 = 16 * ks + q;
-        if (sA0 >= nv) zA0 = 0u;
-        if (sA0 + 4 >= nv) zA1 = 0u;
-        if (sA0 + 8 >= nv) zB0 = 0u;
-        if (sA0 + 12 >= nv) zB1 = 0u;
-      }
-      pv_zeros<D>(acc, zA0, zA1, zB0, zB1, bP[ks][0], bP[ks][1]);
+      const uint32_t zab = pair_h(pw(pa, jz, true), pw(pb, jz, true), ph(jz, true));
+      const uint32_t zcd = pair_h(pw(pc, jz, true), pw(pd, jz, true), ph(jz, true));
+      mma16816_b64(acc.zs, zab, zab, zcd, zcd, pack_b64(bP[ks][0], bP[ks][1]));
     }
 #pragma unroll
-    for (int j = 0; j < C::NGRP; ++j) {
-      const uint32_t rA = prmt(ld_s32(vc, S * (16 * ks) + 16 * j), ld_s32(vc, S * (16 * ks + 4) + 16 * j), selV);
-      const uint32_t rB = prmt(ld_s32(vc, S * (16 * ks + 8) + 16 * j), ld_s32(vc, S * (16 * ks + 12) + 16 * j), selV);
-      uint32_t fA[4], fB[4];
-      fA[0] = hsub2u(lop_and_or(rA, 0x000F000Fu, MAGIC), MAGIC);
-      fA[1] = hsub2u(lop_and_or(rA >> 2, 0x003C003Cu, MAGIC), MAGIC);
-      fA[2] = hsub2u(lop_and_or(rA >> 4, 0x00F000F0u, MAGIC), MAGIC);
-      fA[3] = hsub2u(lop_and_or(rA >> 6, 0x03C003C0u, MAGIC), MAGIC);
-      fB[0] = hsub2u(lop_and_or(rB, 0x000F000Fu, MAGIC), MAGIC);
-      fB[1] = hsub2u(lop_and_or(rB >> 2, 0x003C003Cu, MAGIC), MAGIC);
-      fB[2] = hsub2u(lop_and_or(rB >> 4, 0x00F000F0u, MAGIC), MAGIC);
-      fB[3] = hsub2u(lop_and_or(rB >> 6, 0x03C003C0u, MAGIC), MAGIC);
-      pv_group<D>(acc, j, fA, fB, bP[ks][0], bP[ks][1], pA0[j], pA1[j], pB0[j], pB1[j]);
+    for (int j = 0; j < NG; ++j) {
+      const int vh = NG == 1 ? 0 : (j & 1);
+      const uint32_t rab = pair_h(va[j >> 1], vb[j >> 1], vh), rcd = pair_h(vc[j >> 1], vd[j >> 1], vh);
+      const uint32_t sab = pair_h(pw(pa, j, false), pw(pb, j, false), ph(j, false));
+      const uint32_t scd = pair_h(pw(pc, j, false), pw(pd, j, false), ph(j, false));
+      const uint64_t ps = pack_b64(hmul2u(bP[ks][0], sab), hmul2u(bP[ks][1], scd));
+      // channels 32j + 4g + {0,1,2,3}: lo nibble byte 0 (-> bits 4-7), hi nibble byte 0 (-> 6-9), ...
+      mma16816_b64(acc.o[2 * j], (rab << 4) & M4A, (rab << 2) & M4B, (rcd << 4) & M4A, (rcd << 2) & M4B, ps);
+      mma16816_b64(acc.o[2 * j + 1], (rab >> 4) & M4A, (rab >> 6) & M4B, (rcd >> 4) & M4A, (rcd >> 6) & M4B, ps);
     }
   }
 }
@@ -512,17 +510,32 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
 #pragma unroll
     for (int i = 0; i < C::NCH; ++i) {
-      const int c2 = 16 * i + 4 * q;
-      const int b4 = 32 * (i >> 1) + 8 * q + 2 * (i & 1);
-      const float x0 = qv(c2), x1 = qv(c2 + 1), x2 = qv(c2 + 2), x3 = qv(c2 + 3);
-      const float y0 = qv(b4), y1 = qv(b4 + 4), y2 = qv(b4 + 1), y3 = qv(b4 + 5);
-      qf.b2[i] = pack_b64(pack_h2(x0, x1), pack_h2(x2, x3));
-      qf.b4[i] = pack_b64(pack_h2(y0, y1), pack_h2(y2, y3));
-      if constexpr (LO) {
-        qf.b2lo[i] = pack_b64(pack_h2(lo(x0), lo(x1)), pack_h2(lo(x2), lo(x3)));
-        qf.b4lo[i] = pack_b64(pack_h2(lo(y0), lo(y1)), pack_h2(lo(y2), lo(y3)));
-      }
+      const int cb = q * (D / 4) + 4 * i;
+      const float x0 = qv(cb), x1 = qv(cb + 1), x2 = qv(cb + 2), x3 = qv(cb + 3);
+      qf.b2[i] = pack_b64(pack_h2(x0, x2), pack_h2(x1, x3));
+      if constexpr (LO) qf.b2lo[i] = pack_b64(pack_h2(lo(x0), lo(x2)), pack_h2(lo(x1), lo(x3)));
     }
+    float qa = 0.f, qb = 0.f;  // Q_2q, Q_2q+1 (group sums, fp32)
+#pragma unroll
+    for (int j = 0; j < C::NGRP; ++j) {
+      const int cb = 32 * j + 8 * q;
+      float y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) y[e] = qv(cb + e);
+      qf.b4[2 * j] = pack_b64(pack_h2(y[1], y[5]), pack_h2(y[0], y[4]));
+      qf.b4[2 * j + 1] = pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3], y[7]));
+      if constexpr (LO) {
+        qf.b4lo[2 * j] = pack_b64(pack_h2(lo(y[1]), lo(y[5])), pack_h2(lo(y[0]), lo(y[4])));
+        qf.b4lo[2 * j + 1] = pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]), lo(y[7])));
+      }
+      float part = ((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]));
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (j == 2 * q) qa = part;
+      if (j == 2 * q + 1) qb = part;
+    }
+    qf.qz = pack_b64(pack_h2(qa, qb), 0u);
+    qf.qzlo = pack_b64(pack_h2(lo(qa), lo(qb)), 0u);
   }
 
   Acc<D> acc;
@@ -559,7 +572,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     }
   }
 
-  // ---- finalize this warp: full l per head, acc[h][c] = 2^(10-2e) * O^T + zsum ----
+  // ---- finalize this warp: full l per head, acc[h][c] = 2^20 or 2^18 * O^T + zsum ----
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
     st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, off);
@@ -583,7 +596,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     const int j = m >> 1;
     const int e0 = 2 * (m & 1);
     const int ch0 = 32 * j + 4 * g + e0;
-    const float f0 = (float)(1 << (10 - 2 * e0)), f1 = (float)(1 << (10 - 2 * (e0 + 1)));
+    const float f0 = P20, f1 = P18;  // even channels (rows g) at 2^-20, odd (rows g+8) at 2^-18
     sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, z0[j]);
     sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, z1[j]);
     sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, z0[j]);
@@ -625,11 +638,7 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
   }
   const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)page_stride(D);
   const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)slot_stride(D);
-  auto deq = [](const uint8_t* blk, int c, int bits) {
-    const uint32_t code = (blk[c * bits / 8] >> ((c * bits) & 7)) & ((1u << bits) - 1);
-    const __half2 pz = *reinterpret_cast<const __half2*>(blk + D * bits / 8 + 4 * (c / G));
-    return fmaf((float)code, __low2float(pz), __high2float(pz));
-  };
+  auto hf = [](const uint8_t* p, int idx) { return __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(p)[idx])); };
   for (int t = u.tlo + warp; t < u.thi; t += NW) {
     const bool is2 = t < u.npg;
     const int nrow = is2 ? G : min(32, u.n4 - 32 * (t - u.npg));
@@ -640,10 +649,11 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           const int c = lane + 32 * i;
-          const uint32_t code = (rec[8 * c + r / 4] >> (2 * (r & 3))) & 3u;
-          const __half2 pz = *reinterpret_cast<const __half2*>(rec + 8 * D + 4 * c);
-          kx[i] = fmaf((float)code, __low2float(pz), __high2float(pz));
-          vx[i] = deq(rec + key_page_bytes(D) + r * tok_bytes(D, 2), c, 2);
+          const uint32_t kc = (rec[pg_kc_off(D, r >> 2, c)] >> (2 * (r & 3))) & 3u;
+          kx[i] = fmaf((float)kc, hf(rec + PG_KS(D), pg_kp_idx(c)), hf(rec + PG_KZ(D), pg_kp_idx(c)));
+          const uint32_t vc = (rec[PG_VC(D) + pg_vc_off(D, r, c >> 2)] >> (2 * (c & 3))) & 3u;
+          const int pj = pg_vp_idx(D, r, c / G);
+          vx[i] = fmaf((float)vc, hf(rec + PG_VS(D), pj), hf(rec + PG_VZ(D), pj));
         }
       } else {
         const int64_t slot = a.int4_ids[u.i40 + 32 * (t - u.npg) + r];
@@ -651,8 +661,10 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           const int c = lane + 32 * i;
-          kx[i] = deq(rec, c, 4);
-          vx[i] = deq(rec + tok_bytes(D, 4), c, 4);
+          const uint32_t kc = (rec[sl_kc_off(D, c >> 1)] >> (4 * (c & 1))) & 15u;
+          kx[i] = fmaf((float)kc, hf(rec + SL_KS(D), c / G), hf(rec + SL_KZ(D), c / G));
+          const uint32_t vc = (rec[SL_VC(D) + sl_vc_off(D, c >> 1)] >> (4 * (c & 1))) & 15u;
+          vx[i] = fmaf((float)vc, hf(rec + SL_VS(D), c / G), hf(rec + SL_VZ(D), c / G));
         }
       }
 #pragma unroll

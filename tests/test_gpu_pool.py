@@ -6,6 +6,7 @@ import pytest
 import torch
 
 import paper_2605_17170_b200 as kv
+from paper_2605_17170_b200 import layout
 from oracle import pool as opool
 
 from conftest import rand_kv
@@ -21,9 +22,15 @@ def pool_images(pool):
 
 
 def assert_same_image(pool, op):
+    """Every written record holds exactly the oracle's reference payloads: compared both
+    as reference-order payloads recovered from the device records and as device records."""
+    d = pool.config.head_dim
     i2, i4 = pool_images(pool)
-    assert np.array_equal(i2[op.page_written], op.int2[op.page_written])
-    assert np.array_equal(i4[op.slot_written], op.int4[op.slot_written])
+    pw, sw = op.page_written, op.slot_written
+    assert np.array_equal(layout.page_payloads(i2[pw], d), op.int2[pw])
+    assert np.array_equal(layout.slot_payloads(i4[sw], d), op.int4[sw][:, : 2 * (d // 2 + d // 8)])
+    assert np.array_equal(i2[pw], layout.page_records(op.int2[pw], d))
+    assert np.array_equal(i4[sw], layout.slot_records(op.int4[sw], d))
 
 
 @pytest.mark.parametrize("d,dtype", [(32, torch.float32), (64, torch.bfloat16), (128, torch.float32),
@@ -123,9 +130,9 @@ def test_write_page_and_token(cuda):
     from oracle import codec
     i2, i4 = pool_images(pool)
     exp2 = np.concatenate([codec.encode_key_pages(keys), codec.encode_token_blocks(vals, 2).reshape(-1)])
-    assert np.array_equal(i2[1, 1, 0, : exp2.size], exp2)
+    assert np.array_equal(layout.page_payloads(i2[1, 1, 0], 32), exp2)
     exp4 = np.concatenate([codec.encode_token_blocks(k4[None], 4)[0], codec.encode_token_blocks(-k4[None], 4)[0]])
-    assert np.array_equal(i4[0, 1, 0, : exp4.size], exp4)
+    assert np.array_equal(layout.slot_payloads(i4[0, 1, 0], 32), exp4)
     with pytest.raises(kv.ValidationError):
         pool.write_page(0, np.zeros((16, 32)), np.zeros((16, 32)), 0, 0)
     with pytest.raises(kv.ValidationError):

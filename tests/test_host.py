@@ -44,6 +44,28 @@ def test_abi_strides_and_sizes():
     assert _lib.lib.kvmix_version().startswith(b"kvmix_b200")
 
 
+@pytest.mark.parametrize("d", [32, 64, 128, 256])
+def test_record_layout_matches_kernels(d):
+    """layout.py (numpy statement of the device record permutation) equals the
+    permutation the CUDA kernels compute (exported host-side by the library), and it is
+    a bijection onto the reference payload bytes (every byte kept, nothing re-rounded)."""
+    import ctypes
+    from paper_2605_17170_b200 import layout
+    for fn, pyperm, stride in ((_lib.lib.kvmix_page_layout, layout.page_perm(d), _lib.page_stride(d)),
+                               (_lib.lib.kvmix_slot_layout, layout.slot_perm(d), _lib.slot_stride(d))):
+        out = np.zeros(stride, dtype=np.int64)
+        _lib.check(fn(d, out.ctypes.data_as(ctypes.c_void_p)))
+        assert np.array_equal(out, pyperm)
+    rng = np.random.default_rng(d)
+    ref = rng.integers(0, 256, (3, layout.page_stride(d)), dtype=np.uint8)
+    assert np.array_equal(layout.page_payloads(layout.page_records(ref, d), d), ref)
+    n4 = 2 * kv.token_block_payload_bytes(d, 4)
+    ref4 = rng.integers(0, 256, (3, n4), dtype=np.uint8)
+    rec4 = layout.slot_records(np.concatenate([ref4, np.zeros((3, layout.slot_stride(d) - n4), np.uint8)], 1), d)
+    assert np.array_equal(layout.slot_payloads(rec4, d), ref4)
+    assert not rec4[:, layout.slot_perm(d) < 0].any()
+
+
 def test_abi_validation_without_gpu():
     # argument validation happens before any CUDA call and maps to ValidationError
     rc = _lib.lib.kvmix_encode_token_blocks(None, 1, 33, 2, None, 36, None, None)
