@@ -71,8 +71,8 @@ __device__ __forceinline__ void encode_key_channel(const float (&x)[G], uint8_t*
 #pragma unroll
   for (int tau = 0; tau < 8; ++tau) rec[pg_kc_off(D, tau, c)] = (uint8_t)(((tau < 4 ? w0 : w1) >> (8 * (tau & 3))) & 0xffu);
   const uint32_t pz = pack_param(scale, zero);
-  reinterpret_cast<uint16_t*>(rec + PG_KS(D))[pg_kp_idx(c)] = (uint16_t)(pz & 0xffffu);
-  reinterpret_cast<uint16_t*>(rec + PG_KZ(D))[pg_kp_idx(c)] = (uint16_t)(pz >> 16);
+  reinterpret_cast<uint16_t*>(rec + PG_KS(D))[pg_kp_idx(D, c)] = (uint16_t)(pz & 0xffffu);
+  reinterpret_cast<uint16_t*>(rec + PG_KZ(D))[pg_kp_idx(D, c)] = (uint16_t)(pz >> 16);
 }
 
 // TokenBlock placement inside a staged INT2 page record (token row t of the page).
@@ -353,7 +353,7 @@ __global__ void gather_dequant_kernel(const uint8_t* __restrict__ int2_pool, con
     const int row = (int)(slot % G);
     const uint8_t* rec = int2_pool + ((layer * n_kv_heads + h) * pool_pages + page) * page_stride(D);
     const uint32_t kc = (rec[pg_kc_off(D, row >> 2, c)] >> (2 * (row & 3))) & 3u;
-    kv = __fmaf_rn((float)kc, half_at(rec + PG_KS(D), pg_kp_idx(c)), half_at(rec + PG_KZ(D), pg_kp_idx(c)));
+    kv = __fmaf_rn((float)kc, half_at(rec + PG_KS(D), pg_kp_idx(D, c)), half_at(rec + PG_KZ(D), pg_kp_idx(D, c)));
     const uint32_t vc = (rec[PG_VC(D) + pg_vc_off(D, row, c >> 2)] >> (2 * (c & 3))) & 3u;
     const int pj = pg_vp_idx(D, row, c / G);
     vv = __fmaf_rn((float)vc, half_at(rec + PG_VS(D), pj), half_at(rec + PG_VZ(D), pj));
@@ -393,8 +393,8 @@ extern "C" int kvmix_page_layout(int64_t d, int64_t* perm) {
   for (int c = 0; c < D; ++c) {
     for (int tau = 0; tau < 8; ++tau) perm[pg_kc_off(D, tau, c)] = 8 * c + tau;
     for (int k = 0; k < 2; ++k) {
-      perm[PG_KS(D) + 2 * pg_kp_idx(c) + k] = 8 * D + 4 * c + k;
-      perm[PG_KZ(D) + 2 * pg_kp_idx(c) + k] = 8 * D + 4 * c + 2 + k;
+      perm[PG_KS(D) + 2 * pg_kp_idx(D, c) + k] = 8 * D + 4 * c + k;
+      perm[PG_KZ(D) + 2 * pg_kp_idx(D, c) + k] = 8 * D + 4 * c + 2 + k;
     }
   }
   for (int t = 0; t < G; ++t) {

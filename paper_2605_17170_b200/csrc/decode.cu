@@ -27,10 +27,13 @@
 namespace kvmix {
 
 #ifndef KVMIX_STAGES
-#define KVMIX_STAGES 3
+#define KVMIX_STAGES 2
 #endif
 #ifndef KVMIX_MINB
 #define KVMIX_MINB 3
+#endif
+#ifndef KVMIX_SPLIT
+#define KVMIX_SPLIT 0
 #endif
 constexpr int NW = 4;                 // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
@@ -47,7 +50,7 @@ struct Cfg {
   static constexpr int PS = page_stride(D);
   static constexpr int SS = slot_stride(D);
   static constexpr int BUF = PS > 32 * SS ? PS : 32 * SS;  // one INT2 page or 32 INT4 slots (slot-contiguous)
-  static constexpr int SMEM = NW * STAGES * BUF;
+  static constexpr int SMEM = NW * STAGES * BUF + (D / 8 + 2) * 32 * 8 * 2;  // ring + q fragment table (LO size)
 };
 
 struct DecodeArgs {
@@ -166,7 +169,8 @@ struct Softmax {
 template <int D>
 struct Acc {
   float o[D / 16][4];  // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
-  float zs[4];         // Z^T.P^T: row j (< D/32) = sum_t z_tj p_th (rows >= D/32 unused)
+  float zs[4];         // Z^T.P^T, rows g: row j (< D/32) = sum_t z_tj p_th (rows >= D/32 unused)
+  float zs2[4];        // same sums collected in rows g+8 (INT2 k-step 1, see int2_tile)
 };
 
 __device__ __forceinline__ uint32_t ld_s32(const uint8_t* base, int off) {
@@ -198,6 +202,8 @@ __device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, 
     }
     acc.zs[0] *= al0; acc.zs[2] *= al0;
     acc.zs[1] *= al1; acc.zs[3] *= al1;
+    acc.zs2[0] *= al0; acc.zs2[2] *= al0;
+    acc.zs2[1] *= al1; acc.zs2[3] *= al1;
     st.m0 = mn0;
     st.m1 = mn1;
   }
@@ -258,9 +264,18 @@ constexpr float P20 = 1048576.f, P18 = 262144.f;
 // With LO (fp32 q) the *lo arrays hold q - fp16(q).
 template <int D, bool LO>
 struct QFrag {
-  uint64_t b2[D / 16], b4[D / 16];
-  uint64_t b2lo[LO ? D / 16 : 1], b4lo[LO ? D / 16 : 1];
-  uint64_t qz, qzlo;
+  static constexpr int NCH = D / 16;
+  // fragment index f: b2 [0, NCH), b4 [NCH, 2NCH), qz 2NCH, qzlo 2NCH+1, b2lo / b4lo after
+  static constexpr int F = 2 * NCH + 2 + (LO ? 2 * NCH : 0);
+  static constexpr int BYTES = F * 32 * 8;
+  const uint64_t* p;  // this lane's column of the CTA's [F][32 lanes] fragment table in smem
+  __device__ __forceinline__ uint64_t at(int f) const { return p[f * 32]; }
+  __device__ __forceinline__ uint64_t b2(int i) const { return at(i); }
+  __device__ __forceinline__ uint64_t b4(int i) const { return at(NCH + i); }
+  __device__ __forceinline__ uint64_t qz() const { return at(2 * NCH); }
+  __device__ __forceinline__ uint64_t qzlo() const { return at(2 * NCH + 1); }
+  __device__ __forceinline__ uint64_t b2lo(int i) const { return at(2 * NCH + 2 + i); }
+  __device__ __forceinline__ uint64_t b4lo(int i) const { return at(3 * NCH + 2 + i); }
 };
 
 // ---------------------------------- INT2 page tile ----------------------------------
@@ -279,38 +294,56 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
     const int p = q * KB + o;
     lds_vec<LB>(buf + g * D + ((((p >> 4) ^ (g & 1)) << 4) | (p & 15)), kw + o / 4);
   }
-  lds_vec<2 * KB>(buf + PG_KS(D) + 2 * q * KB, ksw);
-  lds_vec<2 * KB>(buf + PG_KZ(D) + 2 * q * KB, kzw);
-  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, cb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < KB / 8; ++i) {  // 16 B chunk i of lane q at chunk 4i + q
+    lds_vec<16>(buf + PG_KS(D) + (4 * i + q) * 16, ksw + 4 * i);
+    lds_vec<16>(buf + PG_KZ(D) + (4 * i + q) * 16, kzw + 4 * i);
+  }
+  // two accumulators per M tile (even / odd chunks) halve the HMMA dependency chains
+  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, d0[4] = {0.f, 0.f, 0.f, 0.f},
+        d1[4] = {0.f, 0.f, 0.f, 0.f};
+  // bias sum_c q_c z_c: the KZ quad of chunks (2P, 2P+1) is (z_2P.p0, z_2P+1.p0, z_2P.p1, z_2P+1.p1),
+  // used as-is as the A operand: rows g of cbE are chunk 2P's bias, rows g+8 of cbO chunk 2P+1's
+  float cbE[4] = {0.f, 0.f, 0.f, 0.f}, cbO[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < C::NCH; ++i) {
+    const int P4 = 4 * (i >> 1), odd = i & 1;
     const uint32_t w = kw[i], u = w << 4, v = w >> 4, x = w >> 8;
-    const uint64_t qi = qf.b2[i];
-    const uint64_t qs = pack_b64(hmul2u(lo32(qi), ksw[2 * i]), hmul2u(hi32(qi), ksw[2 * i + 1]));
+    const uint64_t qi = qf.b2(i);
+    const uint64_t qs = pack_b64(hmul2u(lo32(qi), ksw[P4 + odd]), hmul2u(hi32(qi), ksw[P4 + 2 + odd]));
+#if KVMIX_SPLIT
+    mma16816_b64(odd ? d0 : c0, u & M2A, u & M2B, v & M2A, v & M2B, qs);
+    mma16816_b64(odd ? d1 : c1, w & M2A, w & M2B, x & M2A, x & M2B, qs);
+#else
     mma16816_b64(c0, u & M2A, u & M2B, v & M2A, v & M2B, qs);
     mma16816_b64(c1, w & M2A, w & M2B, x & M2A, x & M2B, qs);
-    // bias rows g carry sum_c q_c z_c; rows g+8 (cb[2], cb[3]) are don't-care filler
-    mma16816_b64(cb, kzw[2 * i], kzw[2 * i], kzw[2 * i + 1], kzw[2 * i + 1], qi);
-    if constexpr (LO) mma16816_b64(cb, kzw[2 * i], kzw[2 * i], kzw[2 * i + 1], kzw[2 * i + 1], qf.b2lo[i]);
+#endif
+    mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qi);
+    if constexpr (LO) mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qf.b2lo(i));
   }
-  const float b0 = cb[0] * qscale, b1 = cb[1] * qscale;
+  const float b0 = (cbE[0] + cbO[2]) * qscale, b1 = (cbE[1] + cbO[3]) * qscale;
   const float fa = P20 * qscale, fb = P18 * qscale;
-  const float sv[8] = {fmaf(c0[0], fa, b0), fmaf(c0[1], fa, b1), fmaf(c0[2], fb, b0), fmaf(c0[3], fb, b1),
-                       fmaf(c1[0], fa, b0), fmaf(c1[1], fa, b1), fmaf(c1[2], fb, b0), fmaf(c1[3], fb, b1)};
+  const float sv[8] = {fmaf(c0[0] + d0[0], fa, b0), fmaf(c0[1] + d0[1], fa, b1), fmaf(c0[2] + d0[2], fb, b0),
+                       fmaf(c0[3] + d0[3], fb, b1), fmaf(c1[0] + d1[0], fa, b0), fmaf(c1[1] + d1[1], fa, b1),
+                       fmaf(c1[2] + d1[2], fb, b0), fmaf(c1[3] + d1[3], fb, b1)};
   uint32_t bP[2][2];
   softmax_tile<D>(sv, st, acc, bP);
+  // V params: one 16 B quad per (q, group j) = (ks0.p0, ks1.p0, ks0.p1, ks1.p1)
+  uint32_t vs[4 * NG], vz[4];
+#pragma unroll
+  for (int j = 0; j < NG; ++j) lds_vec<16>(buf + PG_VS(D) + (j * 4 + q) * 16, vs + 4 * j);
+  lds_vec<16>(buf + PG_VZ(D) + ((g & (NG - 1)) * 4 + q) * 16, vz);
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
-    uint32_t vw[NG], vs[2 * NG], vz[2];
+    uint32_t vw[NG];
     lds_vec<4 * NG>(buf + PG_VC(D) + ((ks * 8 + g) * 4 + q) * NG * 4, vw);
-    lds_vec<8 * NG>(buf + PG_VS(D) + (ks * 4 + q) * NG * 8, vs);
-    lds_vec<8>(buf + PG_VZ(D) + ((ks * 4 + q) * NG + (g & (NG - 1))) * 8, vz);
-    // sum_t p_th z_tj for all groups at once: A = Z^T (row g = group g & (NG-1)), B = P^T
-    mma16816_b64(acc.zs, vz[0], vz[0], vz[1], vz[1], pack_b64(bP[ks][0], bP[ks][1]));
+    // sum_t p_th z_tj for all groups at once: A = Z^T (row g = group g & (NG-1)), B = P^T.
+    // k-step 0 is valid in rows g (zs), k-step 1 in rows g+8 (zs2) of the same quad.
+    mma16816_b64(ks ? acc.zs2 : acc.zs, vz[0], vz[1], vz[2], vz[3], pack_b64(bP[ks][0], bP[ks][1]));
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
       const uint32_t w = vw[j], u = w << 4, v = w >> 4, x = w >> 8;
-      const uint64_t ps = pack_b64(hmul2u(bP[ks][0], vs[2 * j]), hmul2u(bP[ks][1], vs[2 * j + 1]));
+      const uint64_t ps = pack_b64(hmul2u(bP[ks][0], vs[4 * j + ks]), hmul2u(bP[ks][1], vs[4 * j + 2 + ks]));
       mma16816_b64(acc.o[2 * j], u & M2A, u & M2B, v & M2A, v & M2B, ps);
       mma16816_b64(acc.o[2 * j + 1], w & M2A, w & M2B, x & M2A, x & M2B, ps);
     }
@@ -346,11 +379,11 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
     for (int j = 0; j < NG; ++j) {
       dj[j][0] = dj[j][1] = dj[j][2] = dj[j][3] = 0.f;
       const uint32_t wa = kwa[j], wb = kwb[j];
-      mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4[2 * j]);
-      mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4[2 * j + 1]);
+      mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4(2 * j));
+      mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4(2 * j + 1));
       if constexpr (LO) {
-        mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4lo[2 * j]);
-        mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4lo[2 * j + 1]);
+        mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4lo(2 * j));
+        mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4lo(2 * j + 1));
       }
     }
     // sum_j z_j Q_j: A row = token, k = 2q, 2q+1 -> groups 2q, 2q+1 (lanes with 2q >= NG give 0)
@@ -363,8 +396,8 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
       if (q == 0) { za = pa[0] >> 16; zb = pb[0] >> 16; }
     }
     float zq[4] = {0.f, 0.f, 0.f, 0.f};
-    mma16816_b64(zq, za, zb, 0u, 0u, qf.qz);
-    mma16816_b64(zq, za, zb, 0u, 0u, qf.qzlo);
+    mma16816_b64(zq, za, zb, 0u, 0u, qf.qz());
+    mma16816_b64(zq, za, zb, 0u, 0u, qf.qzlo());
     float ta0 = zq[0] * qscale, ta1 = zq[1] * qscale, tb0 = zq[2] * qscale, tb1 = zq[3] * qscale;
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
@@ -501,19 +534,21 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   }
   int meta_next = load_meta(STAGES);
 
-  // ---- Q fragments (see QFrag) ----
-  QFrag<D, LO> qf;
-  {
+  // ---- Q fragments (see QFrag): built once per CTA by warp 0 into shared memory ----
+  uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + NW * STAGES * C::BUF);
+  if (warp == 0) {
     const bool hv = g < a.gq;
     const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
     auto qv = [&](int c) { return hv ? load_q(a, qrow + c) : 0.f; };
     auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
+    using QF = QFrag<D, LO>;
+    auto put = [&](int f, uint64_t v) { qtab[f * 32 + lane] = v; };
 #pragma unroll
     for (int i = 0; i < C::NCH; ++i) {
       const int cb = q * (D / 4) + 4 * i;
       const float x0 = qv(cb), x1 = qv(cb + 1), x2 = qv(cb + 2), x3 = qv(cb + 3);
-      qf.b2[i] = pack_b64(pack_h2(x0, x2), pack_h2(x1, x3));
-      if constexpr (LO) qf.b2lo[i] = pack_b64(pack_h2(lo(x0), lo(x2)), pack_h2(lo(x1), lo(x3)));
+      put(i, pack_b64(pack_h2(x0, x2), pack_h2(x1, x3)));
+      if constexpr (LO) put(2 * QF::NCH + 2 + i, pack_b64(pack_h2(lo(x0), lo(x2)), pack_h2(lo(x1), lo(x3))));
     }
     float qa = 0.f, qb = 0.f;  // Q_2q, Q_2q+1 (group sums, fp32)
 #pragma unroll
@@ -522,11 +557,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       float y[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) y[e] = qv(cb + e);
-      qf.b4[2 * j] = pack_b64(pack_h2(y[1], y[5]), pack_h2(y[0], y[4]));
-      qf.b4[2 * j + 1] = pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3], y[7]));
+      put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1], y[5]), pack_h2(y[0], y[4])));
+      put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3], y[7])));
       if constexpr (LO) {
-        qf.b4lo[2 * j] = pack_b64(pack_h2(lo(y[1]), lo(y[5])), pack_h2(lo(y[0]), lo(y[4])));
-        qf.b4lo[2 * j + 1] = pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]), lo(y[7])));
+        put(3 * QF::NCH + 2 + 2 * j, pack_b64(pack_h2(lo(y[1]), lo(y[5])), pack_h2(lo(y[0]), lo(y[4]))));
+        put(3 * QF::NCH + 2 + 2 * j + 1, pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]), lo(y[7]))));
       }
       float part = ((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]));
       part += __shfl_xor_sync(0xffffffffu, part, 1);
@@ -534,14 +569,17 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       if (j == 2 * q) qa = part;
       if (j == 2 * q + 1) qb = part;
     }
-    qf.qz = pack_b64(pack_h2(qa, qb), 0u);
-    qf.qzlo = pack_b64(pack_h2(lo(qa), lo(qb)), 0u);
+    put(2 * QF::NCH, pack_b64(pack_h2(qa, qb), 0u));
+    put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
   }
+  __syncthreads();
+  const QFrag<D, LO> qf{qtab + lane};
 
   Acc<D> acc;
 #pragma unroll
   for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
   acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
+  acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
   Softmax st{-INFINITY, -INFINITY, 0.f, 0.f};
 
   int stage = 0;
@@ -588,8 +626,8 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   float z0[C::NGRP], z1[C::NGRP];  // sum_t p z of group j for heads 2q, 2q+1 (from lane (j, q))
 #pragma unroll
   for (int j = 0; j < C::NGRP; ++j) {
-    z0[j] = __shfl_sync(0xffffffffu, acc.zs[0], 4 * j + q);
-    z1[j] = __shfl_sync(0xffffffffu, acc.zs[1], 4 * j + q);
+    z0[j] = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[2], 4 * j + q);
+    z1[j] = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[3], 4 * j + q);
   }
 #pragma unroll
   for (int m = 0; m < C::NCH; ++m) {
@@ -650,7 +688,7 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
         for (int i = 0; i < CPL; ++i) {
           const int c = lane + 32 * i;
           const uint32_t kc = (rec[pg_kc_off(D, r >> 2, c)] >> (2 * (r & 3))) & 3u;
-          kx[i] = fmaf((float)kc, hf(rec + PG_KS(D), pg_kp_idx(c)), hf(rec + PG_KZ(D), pg_kp_idx(c)));
+          kx[i] = fmaf((float)kc, hf(rec + PG_KS(D), pg_kp_idx(D, c)), hf(rec + PG_KZ(D), pg_kp_idx(D, c)));
           const uint32_t vc = (rec[PG_VC(D) + pg_vc_off(D, r, c >> 2)] >> (2 * (c & 3))) & 3u;
           const int pj = pg_vp_idx(D, r, c / G);
           vx[i] = fmaf((float)vc, hf(rec + PG_VS(D), pj), hf(rec + PG_VZ(D), pj));

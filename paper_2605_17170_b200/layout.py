@@ -18,11 +18,13 @@ plus the page's 32 INT2 V TokenBlocks (quant.py:145-262) in slot order::
   KC [0, 8d)     key codes, byte-major: row tau (tokens 4tau..4tau+3) holds code byte
                  tau of every channel word (KeyPage byte 8c + tau); inside a row the
                  16-byte chunks are XOR-swizzled with (tau & 1)
-  KS [8d, 10d)   key scales, fp16, channel order permuted 4m + {0,2,1,3}
+  KS [8d, 10d)   key scales, fp16: lane q owns channels [q d/4, (q+1) d/4) in 8-channel chunks;
+                 chunk i of lane q is chunk 4i + q; channel 8P + 4I + e of a chunk sits
+                 at 4(e&1) + 2I + (e>>1)
   KZ [10d, 12d)  key zeros, same order
   VC [12d, 20d)  value codes: word ((ks*8 + g)*4 + q)*ng + j holds code byte
                  b = 8j + g of tokens [T0, T0+1, T1, T1+1], T0 = 8q + 2ks, T1 = T0 + 4
-  VS [20d, 22d)  value scales: half (((ks*4 + q)*ng + j)*2 + p)*2 + h is the scale of
+  VS [20d, 22d)  value scales: half (((j*4 + q)*2 + p)*2 + ks)*2 + h is the scale of
                  group j of token 8q + 2ks + 4h + p
   VZ [22d, 24d)  value zeros, same order
 
@@ -51,10 +53,12 @@ def slot_stride(d: int) -> int:
     return -(-(d + 8 * (d // 32)) // 16) * 16
 
 
-def _kp_pos(c: int) -> int:
-    """Position of channel c inside KS/KZ: 4m + {0,2,1,3}[e] (the order is its own inverse)."""
+def _kp_pos(d: int, c: int) -> int:
+    """Half index of channel c inside KS/KZ (see the module docstring)."""
+    kb = d // 4  # channels per lane q
+    q, o = divmod(c, kb)
     e = c & 3
-    return (c & ~3) | ((e & 1) << 1) | (e >> 1)
+    return (((o >> 3) * 4 + q) << 3) | ((e & 1) << 2) | (((c >> 2) & 1) << 1) | (e >> 1)
 
 
 @functools.lru_cache(maxsize=None)
@@ -69,7 +73,7 @@ def page_perm(d: int) -> np.ndarray:
             phys = (((c >> 4) ^ (tau & 1)) << 4) | (c & 15)
             perm[tau * d + phys] = 8 * c + tau
     for c in range(d):
-        pos = _kp_pos(c)
+        pos = _kp_pos(d, c)
         for k in range(2):
             perm[8 * d + 2 * pos + k] = 8 * d + 4 * c + k  # scale_c
             perm[10 * d + 2 * pos + k] = 8 * d + 4 * c + 2 + k  # zero_c
@@ -86,7 +90,7 @@ def page_perm(d: int) -> np.ndarray:
             for j in range(ng):
                 for p in range(2):
                     for h in range(2):
-                        idx = (((ks * 4 + q) * ng + j) * 2 + p) * 2 + h
+                        idx = (((j * 4 + q) * 2 + p) * 2 + ks) * 2 + h
                         t = 8 * q + 2 * ks + 4 * h + p
                         for k in range(2):
                             perm[20 * d + 2 * idx + k] = kp + t * tb2 + d // 4 + 4 * j + k
