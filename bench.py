@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--head-dim", type=int, default=128)
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--int2-frac", type=float, default=None, help="override: i.i.d. bits with this INT2 fraction")
-    ap.add_argument("--plan-waves", type=float, default=1.0, help="split planner: target waves of CTAs")
+    ap.add_argument("--ctas-per-sm", type=int, default=3, help="stream-K planner: resident CTAs per SM")
+    ap.add_argument("--int4-weight", type=float, default=1.0, help="stream-K planner: cost weight of INT4 bytes")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-units", type=int, default=0, help="(request, layer) units timed on CPU")
@@ -266,7 +267,7 @@ def build_workload(args, device, rank: int):
         pool.partition(table)
         rids.append(rid)
     torch.cuda.synchronize()
-    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq, waves=args.plan_waves, ctas_per_sm=3)
+    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq, ctas_per_sm=args.ctas_per_sm, int4_weight=args.int4_weight)
     q = torch.randn((L, B, Hq, d), device=device, generator=gen).to(torch.bfloat16)
     out = torch.empty_like(q)
     return pool, batch, q, out, bits
@@ -426,8 +427,8 @@ def run_ours(args):
                    "layers": args.layers, "batch_per_gpu": args.batch, "ctx": args.ctx,
                    "q_heads": args.q_heads, "kv_heads": args.kv_heads, "head_dim": args.head_dim,
                    "parallelism": f"batch-parallel x{world}", "stored_int2_fraction": n2 / ntok,
-                   "l2": "inputs larger than L2 (0.46 GB KV per layer)", "work_items_per_layer": batch.n_work,
-                   "splits_per_unit (cluster size)": batch.splits},
+                   "l2": "inputs larger than L2 (0.46 GB KV per layer)", "schedule": f"stream-K: {batch.n_cta} CTAs, {batch.n_pieces} pieces, "
+                                                                         f"{batch.n_parts} partials per layer"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": "decode_mma_kernel (K2 split decode + fused combine)",
                      "algorithmic_bytes_per_launch": alg_bytes, "k2_ms_per_launch": ms_k2},

@@ -114,11 +114,15 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
  *   q [batch][n_q_heads][d] (q_dtype), out [batch][n_q_heads][d] (out_dtype)
  *   page_indptr[batch+1], page_ids[]: INT2 page list of each partitioned table (table order)
  *   int4_indptr[batch+1], int4_ids[]: INT4 indices of each table's suffix (table order)
- *   work [n_work][4] = {unit = b*Hkv + kvh, tile_lo, tile_hi, reserved}, unit-major with the
- *     same number S = n_work / (batch*Hkv) in 1..8 of splits per unit; the tiles of a unit
- *     are its INT2 pages then ceil(n_int4/32) INT4 tiles of 32 slots (every tile is
- *     bitwidth-homogeneous).  The S CTAs of a unit run as one thread-block cluster and
- *     merge their (m, l, acc) through distributed shared memory.
+ *   The tiles of a unit (request b, kv head h; unit = b*Hkv + h) are its INT2 pages then
+ *   ceil(n_int4/32) INT4 tiles of 32 slots, so every tile is bitwidth-homogeneous.
+ *   work [n_pieces][8] = {unit, tile_lo, tile_hi, slot, part0, nparts, 0, 0}: a piece is a
+ *     contiguous tile range of one unit; slot = -1 if the piece is the whole unit, else its
+ *     partial slot in partials [n_parts][8][d + 2], the unit's partials being slots
+ *     part0 .. part0 + nparts - 1.
+ *   cta_ptr [n_cta + 1]: CTA i runs pieces cta_ptr[i] .. cta_ptr[i+1] (a byte-balanced share
+ *     of the batch, see plan.py); the last CTA to finish a split unit merges its partials.
+ *   counters [batch * Hkv] int32, zero before the first launch; every launch leaves them zero.
  *   variant: 0 = tensor-core kernel (mma.sync m16n8k16), 1 = simple CUDA-core kernel,
  *     2 = data movement only, 3 = compute only on stale smem (measurement; output meaningless)
  * Requires n_q_heads % Hkv == 0 and n_q_heads / Hkv <= 8, d in {32, 64, 128}. */
@@ -126,8 +130,8 @@ int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dt
                        const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
                        int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
                        const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
-                       const int32_t* int4_ids, const int32_t* work, int64_t n_work, float scale, int32_t variant,
-                       void* stream);
+                       const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
+                       float* partials, int32_t* counters, float scale, int32_t variant, void* stream);
 
 /* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
  * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */

@@ -16,7 +16,7 @@ from .attention import (
     merge_partials,
 )
 from .errors import CapacityError, InfeasibleBudgetError, KvmixError, TemplateStructureError, ValidationError
-from .plan import plan_splits
+from .plan import plan_stream
 from .pool import (
     MixedPrecisionPool,
     PageTable,

@@ -50,7 +50,7 @@ _SIGS = {
     "kvmix_append_int4": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P], ctypes.c_int),
     "kvmix_gather_dequant": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P], ctypes.c_int),
     "kvmix_flash_decode": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
-                            _P, _I64, _F, _I32, _P], ctypes.c_int),
+                            _P, _P, _I64, _P, _P, _F, _I32, _P], ctypes.c_int),
     "kvmix_merge_partials": ([_P, _P, _P, _I64, _I64, _P, _P], ctypes.c_int),
 }
 

@@ -4,8 +4,9 @@ Drop-in for the decode half of /root/reference/pkg/src/kvmix/attention.py:
 ``flash_decode`` keeps its signature (:175) and validation order (:188-201) and
 returns a numpy [H, d] float32 array like the reference; ``merge_partials`` (:154)
 and ``SplitPartial`` (:145) keep their meaning.  The work is done by the sm_100a
-kernel K2 of libkvmix_b200 (tensor-core split decode whose last CTA per
-(request, kv head) merges the split partials -- the combine K3 is fused in).
+kernel K2 of libkvmix_b200 (tensor-core split decode; CTAs stream byte-balanced tile
+ranges and the last CTA of a split (request, kv head) merges its partials -- the
+combine K3 is fused in).
 
 ``DecodeBatch`` / ``flash_decode_batched`` are the native hot-path API: a batch of
 requests, one layer per call, q/out as device tensors, page tables resident on the
@@ -24,7 +25,7 @@ import torch
 from . import _lib
 from ._lib import lib
 from .errors import ValidationError
-from .plan import plan_splits
+from .plan import NUM_SMS_B200, plan_stream
 from .pool import MixedPrecisionPool, PageTable, csr_tables, split_partitioned
 
 VARIANT_TENSOR_CORE = 0
@@ -55,7 +56,8 @@ def merge_partials(parts: Sequence[SplitPartial]) -> np.ndarray:
 
 
 class DecodeBatch:
-    """Device-resident CSR page tables + split plan for a request batch."""
+    """Device-resident CSR page tables + stream-K plan (pieces, CTA ranges, partial slots,
+    arrival counters) for a request batch.  One batch is used on one stream at a time."""
 
     def __init__(self, pool: MixedPrecisionPool, request_ids=None, n_q_heads: int | None = None,
                  tables: list | None = None, **plan_kw):
@@ -82,12 +84,24 @@ class DecodeBatch:
             t = pool.device_tables(self.request_ids)
         self.batch = int(t["n_pages"].size)
         self.csr = t
-        work, splits = plan_splits(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride, pool.slot_stride,
-                                   **self.plan_kw)
+        kw = dict(self.plan_kw)
+        if "n_cta" not in kw:
+            n_sm = NUM_SMS_B200
+            if pool.device is not None and pool.device.type == "cuda":
+                n_sm = torch.cuda.get_device_properties(pool.device).multi_processor_count
+            kw["n_cta"] = n_sm * int(kw.pop("ctas_per_sm", 3))
+        else:
+            kw.pop("ctas_per_sm", None)
+        work, cta_ptr, n_parts = plan_stream(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride,
+                                             pool.slot_stride, **kw)
         dev = pool.device
         self.work = torch.as_tensor(work, device=dev)
-        self.n_work = int(work.shape[0])
-        self.splits = int(splits)
+        self.cta_ptr = torch.as_tensor(cta_ptr, device=dev)
+        self.n_cta = int(cta_ptr.size - 1)
+        self.n_pieces = int(work.shape[0])
+        self.n_parts = n_parts
+        self.partials = torch.empty(max(1, n_parts) * 8 * (cfg.head_dim + 2), dtype=torch.float32, device=dev)
+        self.counters = torch.zeros(self.batch * cfg.n_kv_heads, dtype=torch.int32, device=dev)
         self.n_tokens = t["n_pages"] * cfg.page_size + t["n_int4"]
 
     def kv_bytes(self) -> int:
@@ -122,8 +136,9 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
         q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
         pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,
         batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
-        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.n_work, float(scale),
-        int(variant), _lib.stream()))
+        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
+        batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), int(variant),
+        _lib.stream()))
     return out
 
 

@@ -66,9 +66,11 @@ struct DecodeArgs {
   const int32_t* page_ids;
   const int32_t* int4_indptr;
   const int32_t* int4_ids;
-  const int32_t* work;
-  int cluster;  // CTAs (splits) per (request, kv head) unit == thread-block cluster size
-  float qscale;  // softmax scale * log2(e)
+  const int32_t* work;     // pieces [n][8]: unit, tile_lo, tile_hi, slot (-1: whole unit), part0, nparts
+  const int32_t* cta_ptr;  // [grid + 1]: pieces of CTA i are cta_ptr[i] .. cta_ptr[i+1]
+  float* part;             // split partials [n_parts][8][D + 2] (acc[D], m, l; log2 domain)
+  int32_t* counters;       // [batch * n_kv] arrival counters, zero between launches
+  float qscale;            // softmax scale * log2(e)
 };
 
 __device__ __forceinline__ float load_q(const DecodeArgs& a, int64_t idx) {
@@ -78,19 +80,23 @@ __device__ __forceinline__ float load_q(const DecodeArgs& a, int64_t idx) {
 }
 
 // ------------------------------------------------------------------------------------
-// Work-item prologue shared by both kernel variants.
+// A piece is a contiguous tile range of one (request, kv head) unit; a CTA runs the pieces
+// of its byte-balanced share of the whole batch (stream-K style, plan.py).
 struct Unit {
-  int b, kvh, tlo, thi, npg, n4;
+  int b, kvh, unit, tlo, thi, npg, n4, slot, part0, nparts;
   int64_t pg0, i40;
 };
-__device__ __forceinline__ Unit load_unit(const DecodeArgs& a) {
-  const int32_t* wk = a.work + 4 * (int64_t)blockIdx.x;
+__device__ __forceinline__ Unit load_unit(const DecodeArgs& a, int piece) {
+  const int32_t* wk = a.work + 8 * (int64_t)piece;
   Unit u;
-  const int unit = wk[0];
-  u.b = unit / a.n_kv;
-  u.kvh = unit % a.n_kv;
+  u.unit = wk[0];
+  u.b = u.unit / a.n_kv;
+  u.kvh = u.unit % a.n_kv;
   u.tlo = wk[1];
   u.thi = wk[2];
+  u.slot = wk[3];
+  u.part0 = wk[4];
+  u.nparts = wk[5];
   u.pg0 = a.page_indptr[u.b];
   u.npg = a.page_indptr[u.b + 1] - (int)u.pg0;
   u.i40 = a.int4_indptr[u.b];
@@ -104,17 +110,17 @@ __device__ __forceinline__ void store_out(const DecodeArgs& a, int64_t oi, float
   else reinterpret_cast<__half*>(a.out)[oi] = __float2half(v);
 }
 
-// Epilogue shared by both variants (this is K3, the cross-split combine, fused in):
-// 1. merge the NW warps' (m, l, acc) per head through smem into this CTA's state;
-// 2. the `cluster` CTAs that split one (request, kv head) unit form a thread-block
-//    cluster: after a cluster barrier, CTA rank r merges a slice of the unit's outputs
-//    by reading every CTA's state through distributed shared memory (attention.py:154-165).
-// No global partials, no atomics, no second launch.
+// Piece epilogue shared by both variants (K3, the cross-split combine, is fused in):
+// 1. merge the NW warps' (m, l, acc) per head (smem, written by the caller) into the CTA's
+//    state (attention.py:154-165, log2 domain);
+// 2. a piece that covers its whole unit stores the output; otherwise the CTA writes its
+//    partial to slot u.slot, and the last of the unit's u.nparts CTAs to arrive (global
+//    arrival counter, reset by that CTA for the next launch) merges them and stores.
 template <int D>
-__device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit& u, const float* sm_m,
-                                                const float* sm_l, const float* sm_acc, float* cm, float* cl,
-                                                float* cacc) {
+__device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u, const float* sm_m,
+                                             const float* sm_l, const float* sm_acc, int* sm_flag) {
   __syncthreads();
+  const int64_t obase = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq) * D;
   for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
     const int hh = i / D, c = i % D;
     float M = -INFINITY;
@@ -128,35 +134,44 @@ __device__ __forceinline__ void merge_and_store(const DecodeArgs& a, const Unit&
       acc += f * sm_acc[(w * 8 + hh) * D + c];
       l += f * sm_l[w * 8 + hh];
     }
-    if (a.cluster == 1) {
-      store_out(a, ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + hh) * D + c, acc / l);
+    if (u.slot < 0) {
+      store_out(a, obase + i, acc / l);
     } else {
-      cacc[hh * D + c] = acc;
+      float* pp = a.part + ((int64_t)u.slot * 8 + hh) * (D + 2);
+      pp[c] = acc;
       if (c == 0) {
-        cm[hh] = M;
-        cl[hh] = l;
+        pp[D] = M;
+        pp[D + 1] = l;
       }
     }
   }
-  if (a.cluster == 1) return;
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  cluster.sync();  // every CTA of the unit has published its state in smem
-  const int ns = a.cluster, r = (int)cluster.block_rank();
-  for (int i = r * blockDim.x + threadIdx.x; i < a.gq * D; i += ns * blockDim.x) {
-    const int hh = i / D, c = i % D;
-    float M = -INFINITY;
-    for (int k = 0; k < ns; ++k) M = fmaxf(M, cluster.map_shared_rank(cm, k)[hh]);
-    float acc = 0.f, l = 0.f;
-    for (int k = 0; k < ns; ++k) {
-      const float mk = cluster.map_shared_rank(cm, k)[hh];
-      const float f = mk == -INFINITY ? 0.f : fast_exp2(mk - M);
-      acc = fmaf(cluster.map_shared_rank(cacc, k)[hh * D + c], f, acc);
-      l = fmaf(cluster.map_shared_rank(cl, k)[hh], f, l);
-    }
-    store_out(a, ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + hh) * D + c, acc / l);
+  if (u.slot < 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(a.counters + u.unit, 1);
+    const int last = old == u.nparts - 1;
+    if (last) a.counters[u.unit] = 0;  // ready for the next launch (stream order)
+    *sm_flag = last;
   }
-  cluster.sync();  // keep this CTA's smem alive until all ranks have read it
+  __syncthreads();
+  if (!*sm_flag) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
+    const int hh = i / D, c = i % D;
+    const float* p0 = a.part + ((int64_t)u.part0 * 8 + hh) * (D + 2);
+    constexpr int64_t PSTR = 8 * (D + 2);
+    float M = -INFINITY;
+    for (int k = 0; k < u.nparts; ++k) M = fmaxf(M, __ldcg(p0 + k * PSTR + D));
+    float acc = 0.f, l = 0.f;
+    for (int k = 0; k < u.nparts; ++k) {
+      const float mk = __ldcg(p0 + k * PSTR + D);
+      const float f = mk == -INFINITY ? 0.f : fast_exp2(mk - M);
+      acc = fmaf(__ldcg(p0 + k * PSTR + c), f, acc);
+      l = fmaf(__ldcg(p0 + k * PSTR + D + 1), f, l);
+    }
+    store_out(a, obase + i, acc / l);
+  }
 }
 
 // ====================================================================================
@@ -480,8 +495,8 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   __shared__ __align__(8) uint64_t bars[NW][STAGES];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
-  const Unit u = load_unit(a);
   uint8_t* ring = smem + warp * STAGES * C::BUF;
+  __shared__ int sm_flag;
 
   if (lane == 0) {
 #pragma unroll
@@ -489,7 +504,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     fence_mbar_init();
   }
   __syncwarp();
+  int stage = 0;  // ring position and mbarrier phase persist across pieces
+  uint32_t phase = 0;
 
+  for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
+  const Unit u = load_unit(a, piece);
   const int ntiles = u.thi - u.tlo;
   const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
   const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
@@ -529,8 +548,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     }
   };
   if (MEMORY) {
-    int s0 = 0;
-    for (int k = 0; k < STAGES && k < nmine; ++k) issue(k, load_meta(k), s0++);
+    int s0 = stage;  // the ring continues where the previous piece left it
+    for (int k = 0; k < STAGES && k < nmine; ++k) {
+      issue(k, load_meta(k), s0);
+      if (++s0 == STAGES) s0 = 0;
+    }
   }
   int meta_next = load_meta(STAGES);
 
@@ -582,8 +604,6 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
   Softmax st{-INFINITY, -INFINITY, 0.f, 0.f};
 
-  int stage = 0;
-  uint32_t phase = 0;
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
     const uint8_t* buf = ring + stage * C::BUF;
@@ -616,13 +636,10 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, off);
     st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, off);
   }
-  __syncthreads();  // all warps done with their rings -> reuse smem for the merge
+  __syncthreads();  // all warps done with their rings -> reuse ring smem for the merge
   float* sm_acc = reinterpret_cast<float*>(smem);
   float* sm_m = sm_acc + NW * 8 * D;
   float* sm_l = sm_m + NW * 8;
-  float* cta_acc = sm_l + NW * 8;  // this CTA's merged state, read by the cluster
-  float* cta_m = cta_acc + 8 * D;
-  float* cta_l = cta_m + 8;
   float z0[C::NGRP], z1[C::NGRP];  // sum_t p z of group j for heads 2q, 2q+1 (from lane (j, q))
 #pragma unroll
   for (int j = 0; j < C::NGRP; ++j) {
@@ -646,7 +663,9 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     sm_l[warp * 8 + 2 * q] = st.l0;
     sm_l[warp * 8 + 2 * q + 1] = st.l1;
   }
-  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc, cta_m, cta_l, cta_acc);
+  finish_piece<D>(a, u, sm_m, sm_l, sm_acc, &sm_flag);
+  __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
+  }
 }
 
 // ====================================================================================
@@ -658,9 +677,10 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
   __shared__ float qs[8][D];
   __shared__ float sm_acc[NW * 8 * D];
   __shared__ float sm_m[NW * 8], sm_l[NW * 8];
-  __shared__ float cta_acc[8 * D], cta_m[8], cta_l[8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const Unit u = load_unit(a);
+  __shared__ int sm_flag;
+  for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
+  const Unit u = load_unit(a, piece);
   for (int i = threadIdx.x; i < 8 * D; i += blockDim.x) {
     const int hh = i / D, c = i % D;
     qs[hh][c] = hh < a.gq ? load_q(a, ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + hh) * D + c) * a.qscale : 0.f;
@@ -731,34 +751,23 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
       sm_l[warp * 8 + h] = l[h];
     }
   }
-  merge_and_store<D>(a, u, sm_m, sm_l, sm_acc, cta_m, cta_l, cta_acc);
+  finish_piece<D>(a, u, sm_m, sm_l, sm_acc, &sm_flag);
+  __syncthreads();
+  }
 }
 
 template <typename Kern>
-static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_work, int smem, cudaStream_t s) {
+static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_cta, int smem, cudaStream_t s) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)n_work);
-  cfg.blockDim = dim3(NW * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = a.cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
+  kern<<<(unsigned)n_cta, NW * 32, smem, s>>>(a);
   return check_launch("flash_decode");
 }
 
 template <int D>
-static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaStream_t s) {
+static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaStream_t s) {  // n_work = CTAs
   switch (variant) {
     case 0:
       // fp32 q carries bits fp16 cannot hold: add the q - fp16(q) correction MMAs
@@ -800,14 +809,13 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
                                   int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
                                   int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
                                   const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
-                                  int64_t n_work, float scale, int32_t variant, void* stream) {
+                                  const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
+                                  float scale, int32_t variant, void* stream) {
   if (n_kv <= 0 || n_q % n_kv) return fail(KVMIX_EINVAL, "n_heads not a multiple of the pool's n_kv_heads");
   const int64_t gq = n_q / n_kv;
   if (gq > 8) return fail(KVMIX_EINVAL, "GQA group > 8 not supported");
-  if (batch <= 0 || n_work <= 0) return fail(KVMIX_EINVAL, "empty batch or work list");
-  const int64_t units = batch * n_kv;
-  if (n_work % units || n_work / units > 8)
-    return fail(KVMIX_EINVAL, "work list must hold 1..8 splits per (request, kv head), unit-major");
+  if (batch <= 0 || n_cta <= 0 || n_cta > (1 << 20)) return fail(KVMIX_EINVAL, "empty batch or CTA schedule");
+  if (!work || !cta_ptr || !counters) return fail(KVMIX_EINVAL, "work, cta_ptr and counters are required");
   if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
   if (variant < 0 || variant > 3) return fail(KVMIX_EINVAL, "bad variant");
   DecodeArgs a;
@@ -829,13 +837,15 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   a.int4_indptr = int4_indptr;
   a.int4_ids = int4_ids;
   a.work = work;
-  a.cluster = (int)(n_work / units);
+  a.cta_ptr = cta_ptr;
+  a.part = partials;
+  a.counters = counters;
   a.qscale = scale * LOG2E;
   cudaStream_t s = (cudaStream_t)stream;
   switch (d) {
-    case 32: return launch_decode<32>(a, n_work, variant, s);
-    case 64: return launch_decode<64>(a, n_work, variant, s);
-    case 128: return launch_decode<128>(a, n_work, variant, s);
+    case 32: return launch_decode<32>(a, n_cta, variant, s);
+    case 64: return launch_decode<64>(a, n_cta, variant, s);
+    case 128: return launch_decode<128>(a, n_cta, variant, s);
     default: return fail(KVMIX_EINVAL, "decode supports head_dim 32, 64, 128");
   }
 }

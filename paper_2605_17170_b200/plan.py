@@ -1,58 +1,82 @@
-"""Split-K work planner for the decode kernel (host side, O(batch)).
+"""Stream-K work planner for the decode kernel (host side, vectorised numpy).
 
 The reference splits each request's partitioned table into contiguous
-bitwidth-homogeneous chunks of ``split_len`` entries (attention.py:205-208).  On the
-GPU the unit of work is a tile -- one INT2 page (32 tokens, page_stride bytes) or 32
-INT4 slots (32*slot_stride bytes) -- and a work item is a contiguous tile range of one
-(request, kv head).  Splits are sized by bytes so that the whole launch is about
-``waves`` waves of ``ctas_per_sm`` CTAs on every SM, and every split of a unit
-carries about the same number of bytes.
+bitwidth-homogeneous chunks of ``split_len`` entries (attention.py:205-208) and merges
+the per-split partials (attention.py:154-165).  On the GPU the unit of work is a tile --
+one INT2 page (32 tokens, page_stride bytes) or up to 32 INT4 slots (slot_stride bytes
+each) -- so every tile is bitwidth-homogeneous too.  All (request, kv head) units' tiles
+are laid end to end and cut into ``n_cta`` contiguous ranges of equal bytes, one per
+resident CTA (148 SMs x CTAs per SM): every SM streams the same number of bytes whatever
+the mix of request lengths.  Where a cut falls inside a unit, that unit's pieces write
+partials and the last CTA to finish merges them (the fused K3).
 """
 
 from __future__ import annotations
-
-import math
 
 import numpy as np
 
 NUM_SMS_B200 = 148
 
 
-def plan_splits(n_pages, n_int4, n_kv_heads: int, page_stride: int, slot_stride: int,
-                n_sm: int = NUM_SMS_B200, ctas_per_sm: int = 3, waves: float = 1.0,
-                splits: int | None = None, max_splits: int = 8):
-    """Return (work int32 [B*Hkv*S, 4], S).
+def _tile_bytes(n_pages: int, n_int4: int, page_stride: int, slot_stride: int, int4_weight: float) -> np.ndarray:
+    n4t = -(-n_int4 // 32)
+    tb = np.empty(n_pages + n4t, dtype=np.float64)
+    tb[:n_pages] = page_stride
+    if n4t:
+        nv = np.full(n4t, 32, dtype=np.int64)
+        nv[-1] = n_int4 - 32 * (n4t - 1)
+        tb[n_pages:] = nv * slot_stride * int4_weight
+    return tb
 
-    Every (request, kv head) unit gets the same number S of splits (1..8) so the S CTAs of
-    a unit can run as one thread-block cluster and merge through distributed shared
-    memory.  S is chosen so the launch is about ``waves`` waves of ``ctas_per_sm`` CTAs on
-    every SM; each unit's tiles (INT2 pages first, then 32-slot INT4 tiles) are cut into S
-    contiguous ranges of about equal bytes (a range may be empty for very short requests).
-    Rows are (unit = b*Hkv + kvh, tile_lo, tile_hi, 0).
+
+def plan_stream(n_pages, n_int4, n_kv_heads: int, page_stride: int, slot_stride: int,
+                n_cta: int = 3 * NUM_SMS_B200, int4_weight: float = 1.0):
+    """Return (work int32 [n_pieces, 8], cta_ptr int32 [n_cta + 1], n_parts).
+
+    work rows: (unit = b*Hkv + kvh, tile_lo, tile_hi, slot, part0, nparts, 0, 0); slot is
+    -1 when the piece covers its whole unit, else the partial slot (a split unit's pieces
+    use slots part0 .. part0 + nparts - 1).  CTA i runs pieces cta_ptr[i] .. cta_ptr[i+1]
+    in order; a CTA may hold pieces of several short units, or none.
     """
     n_pages = np.asarray(n_pages, dtype=np.int64)
     n_int4 = np.asarray(n_int4, dtype=np.int64)
     B = n_pages.size
     tiles = n_pages + (n_int4 + 31) // 32
-    if np.any(tiles <= 0):
+    if B == 0 or np.any(tiles <= 0):
         raise ValueError("every request needs at least one cached token")
-    units = B * n_kv_heads
-    if splits is None:
-        splits = int(round(n_sm * ctas_per_sm * waves / units))
-    S = int(min(max(splits, 1), max_splits))
-    tile4 = 32 * slot_stride
-    wbytes = n_pages * page_stride + n_int4 * slot_stride
-    rows = np.zeros((B, n_kv_heads, S, 4), dtype=np.int32)
-    for b in range(B):
-        npg, nt = int(n_pages[b]), int(tiles[b])
-        w2 = npg * page_stride
-        cuts = [0]
-        for k in range(1, S):
-            pos = wbytes[b] * k / S
-            t = int(round(pos / page_stride)) if pos <= w2 else npg + int(round((pos - w2) / tile4))
-            cuts.append(min(max(t, cuts[-1]), nt))
-        cuts.append(nt)
-        rows[b, :, :, 1] = cuts[:-1]
-        rows[b, :, :, 2] = cuts[1:]
-    rows[:, :, :, 0] = (np.arange(B)[:, None, None] * n_kv_heads + np.arange(n_kv_heads)[None, :, None])
-    return rows.reshape(-1, 4), S
+    H = int(n_kv_heads)
+    per_req = [_tile_bytes(int(n_pages[b]), int(n_int4[b]), page_stride, slot_stride, int4_weight)
+               for b in range(B)]
+    unit_tiles = np.repeat(tiles, H)  # unit-major: u = b*H + h
+    ustart = np.zeros(B * H + 1, dtype=np.int64)
+    np.cumsum(unit_tiles, out=ustart[1:])
+    total_tiles = int(ustart[-1])
+    cum = np.cumsum(np.concatenate([np.tile(t, H) for t in per_req]))
+    n_cta = int(max(1, min(n_cta, total_tiles)))
+    target = cum[-1] * np.arange(1, n_cta) / n_cta
+    idx = np.searchsorted(cum, target, side="left")  # cum[idx] >= target
+    prev = np.where(idx > 0, cum[np.maximum(idx - 1, 0)], 0.0)
+    cuts = np.where(cum[idx] - target < target - prev, idx + 1, idx)  # nearest tile boundary
+    cuts = np.maximum.accumulate(np.concatenate([[0], cuts, [total_tiles]])).astype(np.int64)
+    bounds = np.union1d(cuts, ustart)
+    lo, hi = bounds[:-1], bounds[1:]
+    unit = np.searchsorted(ustart, lo, side="right") - 1
+    cta = np.searchsorted(cuts, lo, side="right") - 1
+    cta = np.minimum(cta, n_cta - 1)
+    npieces = np.bincount(unit, minlength=B * H)
+    first = np.searchsorted(unit, np.arange(B * H), side="left")
+    split = npieces > 1
+    part0 = np.zeros(B * H, dtype=np.int64)
+    part0[split] = np.concatenate([[0], np.cumsum(npieces[split])[:-1]])
+    n_parts = int(npieces[split].sum())
+    rank = np.arange(lo.size) - first[unit]
+    work = np.zeros((lo.size, 8), dtype=np.int32)
+    work[:, 0] = unit
+    work[:, 1] = lo - ustart[unit]
+    work[:, 2] = hi - ustart[unit]
+    work[:, 3] = np.where(split[unit], part0[unit] + rank, -1)
+    work[:, 4] = np.where(split[unit], part0[unit], 0)
+    work[:, 5] = npieces[unit]
+    cta_ptr = np.zeros(n_cta + 1, dtype=np.int32)
+    np.cumsum(np.bincount(cta, minlength=n_cta), out=cta_ptr[1:])
+    return work, cta_ptr, n_parts

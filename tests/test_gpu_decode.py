@@ -90,12 +90,16 @@ def test_split_invariance_and_validation(cuda):
         assert np.array_equal(o, outs[0])
     qd = torch.as_tensor(q, device=cuda)[None]
     ref = outs[0]
-    # other split counts change which warp sees which tiles (running max, fp16 rounding of
-    # p*s), so agreement is to ~1e-4 -- an order of magnitude inside the parity tolerance
-    for S in range(1, 9):
-        b = kv.DecodeBatch(pool, ["req"], n_q_heads=4, splits=S)
-        o = kv.flash_decode_batched(qd, b, 0).cpu().numpy()[0]
-        assert np.allclose(o, ref, rtol=2e-3, atol=2e-4), (S, float(np.abs(o - ref).max()))
+    # other CTA counts change the stream-K cuts (which CTA / warp sees which tiles, how many
+    # partials a unit merges, several units per CTA when n_cta < units): the running max and
+    # fp16 rounding of p*s move, so agreement is to ~1e-4 -- well inside the parity tolerance.
+    # Each plan runs twice: the arrival counters must be left at zero by every launch.
+    for n_cta in (1, 2, 3, 5, 8, 13, 64, 444):
+        b = kv.DecodeBatch(pool, ["req"], n_q_heads=4, n_cta=n_cta)
+        for rep in range(2):
+            o = kv.flash_decode_batched(qd, b, 0).cpu().numpy()[0]
+            assert np.allclose(o, ref, rtol=2e-3, atol=2e-4), (n_cta, rep, float(np.abs(o - ref).max()))
+        assert int(b.counters.abs().sum()) == 0
     with pytest.raises(kv.ValidationError):
         kv.flash_decode(q, t, pool.view(0), split_len=0)
     with pytest.raises(kv.ValidationError):

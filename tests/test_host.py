@@ -10,7 +10,7 @@ import pytest
 
 import paper_2605_17170_b200 as kv
 from paper_2605_17170_b200 import _lib
-from paper_2605_17170_b200.plan import plan_splits
+from paper_2605_17170_b200.plan import plan_stream
 from paper_2605_17170_b200.pool import csr_tables, split_partitioned
 from oracle import pool as opool
 
@@ -72,7 +72,7 @@ def test_abi_validation_without_gpu():
     with pytest.raises(kv.ValidationError):
         _lib.check(rc)
     rc = _lib.lib.kvmix_flash_decode(None, 0, None, 0, None, None, 1, 1, 0, 3, 128, 8, 1, None, None, None, None,
-                                     None, 3, 1.0, 0, None)
+                                     None, None, 3, None, None, 1.0, 0, None)
     with pytest.raises(kv.ValidationError, match="multiple"):
         _lib.check(rc)
 
@@ -211,32 +211,50 @@ def test_stats_accounting():
     assert st["int2"]["live"] == 64 and st["int4"]["live"] == 36
 
 
-# ---- split planner --------------------------------------------------------------------------
-@pytest.mark.parametrize("B,Hkv", [(1, 2), (16, 8), (64, 8), (3, 1)])
-def test_plan_covers_every_tile(B, Hkv):
+# ---- stream-K planner -------------------------------------------------------------------------
+def _tile_bytes(npg, n4):
+    n4t = -(-n4 // 32)
+    return [3072] * npg + [160 * min(32, n4 - 32 * k) for k in range(n4t)]
+
+
+@pytest.mark.parametrize("B,Hkv,n_cta", [(1, 2, 444), (16, 8, 444), (64, 8, 444), (3, 1, 7), (5, 2, 1000)])
+def test_plan_covers_every_tile_once(B, Hkv, n_cta):
+    """Every tile of every (request, kv head) is in exactly one piece; pieces of a split
+    unit own consecutive partial slots; CTA ranges are contiguous and in order."""
     rng = np.random.default_rng(B)
     npg = rng.integers(0, 1200, B)
     n4 = rng.integers(0, 5000, B)
     n4[npg == 0] += 1
-    work, S = plan_splits(npg, n4, Hkv, 3072, 160)
-    assert 1 <= S <= 8 and work.shape == (B * Hkv * S, 4)
-    w = work.reshape(B, Hkv, S, 4)
+    work, cta_ptr, n_parts = plan_stream(npg, n4, Hkv, 3072, 160, n_cta=n_cta)
     tiles = npg + (n4 + 31) // 32
-    for b in range(B):
-        for h in range(Hkv):
-            assert (w[b, h, :, 0] == b * Hkv + h).all()
-            assert w[b, h, 0, 1] == 0 and w[b, h, -1, 2] == tiles[b]
-            assert (w[b, h, 1:, 1] == w[b, h, :-1, 2]).all() and (w[b, h, :, 2] >= w[b, h, :, 1]).all()
+    assert cta_ptr[0] == 0 and cta_ptr[-1] == work.shape[0] and (np.diff(cta_ptr) >= 0).all()
+    seen = {}
+    for row in work:
+        u, lo, hi, slot, p0, npc = row[:6]
+        assert 0 <= lo < hi <= tiles[u // Hkv]
+        seen.setdefault(int(u), []).append((int(lo), int(hi), int(slot), int(p0), int(npc)))
+    assert sorted(seen) == list(range(B * Hkv))
+    slots = []
+    for u, pcs in seen.items():
+        assert pcs[0][0] == 0 and pcs[-1][1] == tiles[u // Hkv]
+        assert all(pcs[k][1] == pcs[k + 1][0] for k in range(len(pcs) - 1))
+        assert all(p[4] == len(pcs) for p in pcs)
+        if len(pcs) == 1:
+            assert pcs[0][2] == -1
+        else:
+            assert [p[2] for p in pcs] == list(range(pcs[0][3], pcs[0][3] + len(pcs)))
+            slots += [p[2] for p in pcs]
+    assert sorted(slots) == list(range(n_parts))
 
 
 def test_plan_byte_balance():
-    work, S = plan_splits(np.array([1000] * 16), np.array([6000] * 16), 8, 3072, 160, splits=4)
-    w = work.reshape(16, 8, 4, 4)[0, 0]
-    sizes = []
-    for lo, hi in w[:, 1:3]:
-        b = sum(3072 if t < 1000 else 32 * 160 for t in range(lo, hi))
-        sizes.append(b)
-    assert max(sizes) / min(sizes) < 1.05
+    npg, n4 = np.array([1000] * 16), np.array([6000] * 16)
+    work, cta_ptr, _ = plan_stream(npg, n4, 8, 3072, 160, n_cta=444)
+    per_cta = np.zeros(444)
+    for c in range(444):
+        for u, lo, hi in work[cta_ptr[c]:cta_ptr[c + 1], :3]:
+            per_cta[c] += sum(_tile_bytes(1000, 6000)[lo:hi])
+    assert per_cta.max() / per_cta.mean() < 1.02 and per_cta.min() / per_cta.mean() > 0.98
 
 
 def test_csr_tables_cpu():
