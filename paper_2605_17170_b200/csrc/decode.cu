@@ -262,14 +262,16 @@ __device__ __forceinline__ float half_f(uint32_t w, int hi) {
   return __half2float(__ushort_as_half((unsigned short)(hi ? w >> 16 : w & 0xffffu)));
 }
 
-// Codes enter the MMA as fp16 SUBNORMALS: a 2-bit field masked into mantissa bits 4-5
-// is code * 2^-20, bits 6-7 code * 2^-18 (INT4 nibbles: bits 4-7 -> 2^-20, 6-9 -> 2^-18).
-// One LOP3 per two codes, no magic-number subtraction; the power of two is undone in
-// fp32 per row.  Mantissa bits >= 4 keep the tensor core's subnormal products within
-// ~5e-6 of exact (measured, tools/microbench/denorm.cu); bits 0-3 would not.
-constexpr uint32_t M2A = 0x00300030u, M2B = 0x00C000C0u;  // INT2 field at bits 4-5 / 6-7
-constexpr uint32_t M4A = 0x00F000F0u, M4B = 0x03C003C0u;  // INT4 nibble at bits 4-7 / 6-9
-constexpr float P20 = 1048576.f, P18 = 262144.f;
+// Codes enter the MMA as fp16 SUBNORMALS, masked in place: INT2 field e of a code byte
+// (bits 2e..2e+1) is code * 2^(2e-24); an INT4 low / high nibble is code * 2^-24 / 2^-20.
+// One LOP3 per two codes (plus one shift per 16 codes for the odd bytes), no magic-number
+// subtraction; the power of two is undone in fp32 per row.  The tensor core sums
+// subnormal products with a relative error <= ~8e-5 of the summed magnitudes at bit 0
+// (exact single products; tools/microbench/denorm*.cu), 6x below the fp16 rounding of
+// the q' = q*s operand that the reference's fp32 path does not have.
+__device__ __forceinline__ constexpr uint32_t F2(int e) { return 0x00030003u << (2 * e); }  // INT2 field e
+constexpr uint32_t N4L = 0x000F000Fu, N4H = 0x00F000F0u;  // INT4 low / high nibble of bytes 0, 2
+constexpr float P24 = 16777216.f, P22 = 4194304.f, P20 = 1048576.f, P18 = 262144.f;
 
 // Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).
 //  b2[I]  INT2 key pages, chunk I, lane q: channels cb = q*D/4 + 4I: (cb, cb+2) / (cb+1, cb+3)
@@ -323,24 +325,24 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
 #pragma unroll
   for (int i = 0; i < C::NCH; ++i) {
     const int P4 = 4 * (i >> 1), odd = i & 1;
-    const uint32_t w = kw[i], u = w << 4, v = w >> 4, x = w >> 8;
+    const uint32_t w = kw[i], x = w >> 8;
     const uint64_t qi = qf.b2(i);
     const uint64_t qs = pack_b64(hmul2u(lo32(qi), ksw[P4 + odd]), hmul2u(hi32(qi), ksw[P4 + 2 + odd]));
 #if KVMIX_SPLIT
-    mma16816_b64(odd ? d0 : c0, u & M2A, u & M2B, v & M2A, v & M2B, qs);
-    mma16816_b64(odd ? d1 : c1, w & M2A, w & M2B, x & M2A, x & M2B, qs);
+    mma16816_b64(odd ? d0 : c0, w & F2(0), w & F2(1), x & F2(0), x & F2(1), qs);
+    mma16816_b64(odd ? d1 : c1, w & F2(2), w & F2(3), x & F2(2), x & F2(3), qs);
 #else
-    mma16816_b64(c0, u & M2A, u & M2B, v & M2A, v & M2B, qs);
-    mma16816_b64(c1, w & M2A, w & M2B, x & M2A, x & M2B, qs);
+    mma16816_b64(c0, w & F2(0), w & F2(1), x & F2(0), x & F2(1), qs);
+    mma16816_b64(c1, w & F2(2), w & F2(3), x & F2(2), x & F2(3), qs);
 #endif
     mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qi);
     if constexpr (LO) mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qf.b2lo(i));
   }
   const float b0 = (cbE[0] + cbO[2]) * qscale, b1 = (cbE[1] + cbO[3]) * qscale;
-  const float fa = P20 * qscale, fb = P18 * qscale;
-  const float sv[8] = {fmaf(c0[0] + d0[0], fa, b0), fmaf(c0[1] + d0[1], fa, b1), fmaf(c0[2] + d0[2], fb, b0),
-                       fmaf(c0[3] + d0[3], fb, b1), fmaf(c1[0] + d1[0], fa, b0), fmaf(c1[1] + d1[1], fa, b1),
-                       fmaf(c1[2] + d1[2], fb, b0), fmaf(c1[3] + d1[3], fb, b1)};
+  const float f0 = P24 * qscale, f1 = P22 * qscale, f2 = P20 * qscale, f3 = P18 * qscale;
+  const float sv[8] = {fmaf(c0[0] + d0[0], f0, b0), fmaf(c0[1] + d0[1], f0, b1), fmaf(c0[2] + d0[2], f1, b0),
+                       fmaf(c0[3] + d0[3], f1, b1), fmaf(c1[0] + d1[0], f2, b0), fmaf(c1[1] + d1[1], f2, b1),
+                       fmaf(c1[2] + d1[2], f3, b0), fmaf(c1[3] + d1[3], f3, b1)};
   uint32_t bP[2][2];
   softmax_tile<D>(sv, st, acc, bP);
   // V params: one 16 B quad per (q, group j) = (ks0.p0, ks1.p0, ks0.p1, ks1.p1)
@@ -357,10 +359,10 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
     mma16816_b64(ks ? acc.zs2 : acc.zs, vz[0], vz[1], vz[2], vz[3], pack_b64(bP[ks][0], bP[ks][1]));
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
-      const uint32_t w = vw[j], u = w << 4, v = w >> 4, x = w >> 8;
+      const uint32_t w = vw[j], x = w >> 8;
       const uint64_t ps = pack_b64(hmul2u(bP[ks][0], vs[4 * j + ks]), hmul2u(bP[ks][1], vs[4 * j + 2 + ks]));
-      mma16816_b64(acc.o[2 * j], u & M2A, u & M2B, v & M2A, v & M2B, ps);
-      mma16816_b64(acc.o[2 * j + 1], w & M2A, w & M2B, x & M2A, x & M2B, ps);
+      mma16816_b64(acc.o[2 * j], w & F2(0), w & F2(1), x & F2(0), x & F2(1), ps);
+      mma16816_b64(acc.o[2 * j + 1], w & F2(2), w & F2(3), x & F2(2), x & F2(3), ps);
     }
   }
 }
@@ -378,7 +380,7 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
   using C = Cfg<D>;
   constexpr int S = C::SS, NG = C::NGRP;
   const int g = lane >> 2, q = lane & 3;
-  const float fs = P20 * qscale;
+  const float fs = P24 * qscale;  // every INT4 K product is at 2^-24 (high-nibble q is pre-divided by 16)
   float sv[8];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
@@ -394,11 +396,12 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
     for (int j = 0; j < NG; ++j) {
       dj[j][0] = dj[j][1] = dj[j][2] = dj[j][3] = 0.f;
       const uint32_t wa = kwa[j], wb = kwb[j];
-      mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4(2 * j));
-      mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4(2 * j + 1));
+      const uint32_t xa = wa >> 8, xb = wb >> 8;
+      mma16816_b64(dj[j], wa & N4H, wb & N4H, wa & N4L, wb & N4L, qf.b4(2 * j));
+      mma16816_b64(dj[j], xa & N4L, xb & N4L, xa & N4H, xb & N4H, qf.b4(2 * j + 1));
       if constexpr (LO) {
-        mma16816_b64(dj[j], wa & M4A, wb & M4A, (wa << 4) & M4A, (wb << 4) & M4A, qf.b4lo(2 * j));
-        mma16816_b64(dj[j], (wa >> 4) & M4A, (wb >> 4) & M4A, (wa >> 8) & M4A, (wb >> 8) & M4A, qf.b4lo(2 * j + 1));
+        mma16816_b64(dj[j], wa & N4H, wb & N4H, wa & N4L, wb & N4L, qf.b4lo(2 * j));
+        mma16816_b64(dj[j], xa & N4L, xb & N4L, xa & N4H, xb & N4H, qf.b4lo(2 * j + 1));
       }
     }
     // sum_j z_j Q_j: A row = token, k = 2q, 2q+1 -> groups 2q, 2q+1 (lanes with 2q >= NG give 0)
@@ -481,9 +484,10 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
       const uint32_t sab = pair_h(pw(pa, j, false), pw(pb, j, false), ph(j, false));
       const uint32_t scd = pair_h(pw(pc, j, false), pw(pd, j, false), ph(j, false));
       const uint64_t ps = pack_b64(hmul2u(bP[ks][0], sab), hmul2u(bP[ks][1], scd));
-      // channels 32j + 4g + {0,1,2,3}: lo nibble byte 0 (-> bits 4-7), hi nibble byte 0 (-> 6-9), ...
-      mma16816_b64(acc.o[2 * j], (rab << 4) & M4A, (rab << 2) & M4B, (rcd << 4) & M4A, (rcd << 2) & M4B, ps);
-      mma16816_b64(acc.o[2 * j + 1], (rab >> 4) & M4A, (rab >> 6) & M4B, (rcd >> 4) & M4A, (rcd >> 6) & M4B, ps);
+      // channels 32j + 4g + {0,1,2,3} = nibbles at bits 0, 4, 8, 12 -> bits 0, 2, 4, 6 (INT2 row scales)
+      constexpr uint32_t S0 = 0x000F000Fu, S1 = 0x003C003Cu, S2 = 0x00F000F0u, S3 = 0x03C003C0u;
+      mma16816_b64(acc.o[2 * j], rab & S0, (rab >> 2) & S1, rcd & S0, (rcd >> 2) & S1, ps);
+      mma16816_b64(acc.o[2 * j + 1], (rab >> 4) & S2, (rab >> 6) & S3, (rcd >> 4) & S2, (rcd >> 6) & S3, ps);
     }
   }
 }
@@ -579,11 +583,15 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       float y[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) y[e] = qv(cb + e);
-      put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1], y[5]), pack_h2(y[0], y[4])));
-      put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3], y[7])));
+      // high-nibble channels (cb+1, cb+5, cb+3, cb+7) enter at 2^-20: their q is divided by 16
+      constexpr float R16 = 0.0625f;
+      put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1] * R16, y[5] * R16), pack_h2(y[0], y[4])));
+      put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3] * R16, y[7] * R16)));
       if constexpr (LO) {
-        put(3 * QF::NCH + 2 + 2 * j, pack_b64(pack_h2(lo(y[1]), lo(y[5])), pack_h2(lo(y[0]), lo(y[4]))));
-        put(3 * QF::NCH + 2 + 2 * j + 1, pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]), lo(y[7]))));
+        put(3 * QF::NCH + 2 + 2 * j,
+            pack_b64(pack_h2(lo(y[1]) * R16, lo(y[5]) * R16), pack_h2(lo(y[0]), lo(y[4]))));
+        put(3 * QF::NCH + 2 + 2 * j + 1,
+            pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]) * R16, lo(y[7]) * R16)));
       }
       float part = ((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]));
       part += __shfl_xor_sync(0xffffffffu, part, 1);
@@ -651,7 +659,8 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     const int j = m >> 1;
     const int e0 = 2 * (m & 1);
     const int ch0 = 32 * j + 4 * g + e0;
-    const float f0 = P20, f1 = P18;  // even channels (rows g) at 2^-20, odd (rows g+8) at 2^-18
+    // channel 4g + e of group j carries 2^(2e-24): e = 0/1 in even M tiles, 2/3 in odd ones
+    const float f0 = (m & 1) ? P20 : P24, f1 = (m & 1) ? P18 : P22;
     sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, z0[j]);
     sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, z1[j]);
     sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, z0[j]);
