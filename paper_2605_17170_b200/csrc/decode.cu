@@ -177,39 +177,43 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
 // ====================================================================================
 // Variant 0: tensor-core kernel.  Tile bodies are specialised per bitwidth so that all
 // shared-memory addresses are a lane-constant base plus compile-time immediates.
+// Running max per head (log2 domain) for heads 2q, 2q+1.  Tile logits arrive already
+// shifted by it.  The softmax sum l is not kept here: it is a "ones" row of the
+// zero-point MMA (Acc::zs), so it sums exactly the fp16 p the PV MMAs use.
 struct Softmax {
-  float m0, m1, l0, l1;  // running max / sum for heads 2q, 2q+1 (log2 domain)
+  float m0, m1;
+  bool init;  // false until the warp's first tile of the piece set the max
 };
 
 template <int D>
 struct Acc {
   float o[D / 16][4];  // O^T accumulators (rows = channels, cols = heads 2q, 2q+1)
-  float zs[4];         // Z^T.P^T, rows g: row j (< D/32) = sum_t z_tj p_th (rows >= D/32 unused)
-  float zs2[4];        // same sums collected in rows g+8 (INT2 k-step 1, see int2_tile)
+  float zs[4];   // Z^T.P^T, rows g: row j < D/32 = sum_t z_tj p_th; rows D/32..7 = sum_t p_th (l)
+  float zs2[4];  // same sums for INT2 k-step 1 (group rows in g+8, l rows in g; see int2_tile)
 };
 
 __device__ __forceinline__ uint32_t ld_s32(const uint8_t* base, int off) {
   return *reinterpret_cast<const uint32_t*>(base + off);
 }
 
-// Online softmax over one 32-token tile; returns the P^T B fragments of PV k-steps 0, 1.
+// Online softmax over one 32-token tile.  sv holds the logits minus the running max;
+// returns the P^T B fragments of PV k-steps 0, 1.  Lazy rescale: the max is only raised
+// when some logit exceeds it by > RESCALE_SLACK (log2 units), so p <= 2^RESCALE_SLACK
+// stays well inside fp16 and the common path needs no cross-lane reduction -- only a
+// per-lane max and one vote.  The first tile of a piece establishes the max exactly.
 template <int D>
-__device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, Acc<D>& acc, uint32_t (&bP)[2][2]) {
+__device__ __forceinline__ void softmax_tile(float (&sv)[8], Softmax& st, Acc<D>& acc, uint32_t (&bP)[2][2]) {
   float tm0 = fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6]));
   float tm1 = fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7]));
+  if (__any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK)) {
 #pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
-    tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
-  }
-  // Lazy rescale: keep the stale running max until a tile exceeds it by > RESCALE_SLACK
-  // (log2 units); p then stays <= 2^RESCALE_SLACK, well inside fp16, and the exact
-  // rescale happens only when needed (rarely after the first tiles).
-  if (__any_sync(0xffffffffu, (tm0 > st.m0 + RESCALE_SLACK) || (tm1 > st.m1 + RESCALE_SLACK))) {
-    const float mn0 = fmaxf(st.m0, tm0), mn1 = fmaxf(st.m1, tm1);
-    const float al0 = fast_exp2(st.m0 - mn0), al1 = fast_exp2(st.m1 - mn1);  // exp2(-inf) = 0
-    st.l0 *= al0;
-    st.l1 *= al1;
+    for (int off = 4; off < 32; off <<= 1) {
+      tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
+      tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
+    }
+    // first tile: shift to its max (acc is still zero); later: raise only, by max(tm, 0)
+    const float sh0 = st.init ? fmaxf(tm0, 0.f) : tm0, sh1 = st.init ? fmaxf(tm1, 0.f) : tm1;
+    const float al0 = st.init ? fast_exp2(-sh0) : 0.f, al1 = st.init ? fast_exp2(-sh1) : 0.f;
 #pragma unroll
     for (int m = 0; m < D / 16; ++m) {
       acc.o[m][0] *= al0; acc.o[m][2] *= al0;
@@ -219,18 +223,18 @@ __device__ __forceinline__ void softmax_tile(const float (&sv)[8], Softmax& st, 
     acc.zs[1] *= al1; acc.zs[3] *= al1;
     acc.zs2[0] *= al0; acc.zs2[2] *= al0;
     acc.zs2[1] *= al1; acc.zs2[3] *= al1;
-    st.m0 = mn0;
-    st.m1 = mn1;
+    st.m0 += sh0;
+    st.m1 += sh1;
+    st.init = true;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      sv[i] -= sh0;
+      sv[i + 1] -= sh1;
+    }
   }
-  const float mn0 = st.m0, mn1 = st.m1;
   float p[8];
 #pragma unroll
-  for (int i = 0; i < 8; i += 2) {
-    p[i] = fast_exp2(sv[i] - mn0);
-    p[i + 1] = fast_exp2(sv[i + 1] - mn1);
-  }
-  st.l0 += (p[0] + p[2]) + (p[4] + p[6]);
-  st.l1 += (p[1] + p[3]) + (p[5] + p[7]);
+  for (int i = 0; i < 8; ++i) p[i] = fast_exp2(sv[i]);
   // k index of PV == QK row: lane holds head g, rows (2q, 2q+1) / (2q+8, 2q+9)
   bP[0][0] = movtrans(pack_h2(p[0], p[1]));
   bP[0][1] = movtrans(pack_h2(p[2], p[3]));
@@ -271,6 +275,7 @@ __device__ __forceinline__ float half_f(uint32_t w, int hi) {
 // the q' = q*s operand that the reference's fp32 path does not have.
 __device__ __forceinline__ constexpr uint32_t F2(int e) { return 0x00030003u << (2 * e); }  // INT2 field e
 constexpr uint32_t N4L = 0x000F000Fu, N4H = 0x00F000F0u;  // INT4 low / high nibble of bytes 0, 2
+constexpr uint32_t ONES = 0x3C003C00u;  // (1.0, 1.0) fp16
 constexpr float P24 = 16777216.f, P22 = 4194304.f, P20 = 1048576.f, P18 = 262144.f;
 
 // Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).
@@ -338,9 +343,9 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
     mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qi);
     if constexpr (LO) mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qf.b2lo(i));
   }
-  const float b0 = (cbE[0] + cbO[2]) * qscale, b1 = (cbE[1] + cbO[3]) * qscale;
+  const float b0 = fmaf(cbE[0] + cbO[2], qscale, -st.m0), b1 = fmaf(cbE[1] + cbO[3], qscale, -st.m1);
   const float f0 = P24 * qscale, f1 = P22 * qscale, f2 = P20 * qscale, f3 = P18 * qscale;
-  const float sv[8] = {fmaf(c0[0] + d0[0], f0, b0), fmaf(c0[1] + d0[1], f0, b1), fmaf(c0[2] + d0[2], f1, b0),
+  float sv[8] = {fmaf(c0[0] + d0[0], f0, b0), fmaf(c0[1] + d0[1], f0, b1), fmaf(c0[2] + d0[2], f1, b0),
                        fmaf(c0[3] + d0[3], f1, b1), fmaf(c1[0] + d1[0], f2, b0), fmaf(c1[1] + d1[1], f2, b1),
                        fmaf(c1[2] + d1[2], f3, b0), fmaf(c1[3] + d1[3], f3, b1)};
   uint32_t bP[2][2];
@@ -350,6 +355,7 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
 #pragma unroll
   for (int j = 0; j < NG; ++j) lds_vec<16>(buf + PG_VS(D) + (j * 4 + q) * 16, vs + 4 * j);
   lds_vec<16>(buf + PG_VZ(D) + ((g & (NG - 1)) * 4 + q) * 16, vz);
+  if (g >= NG) vz[0] = vz[1] = vz[2] = vz[3] = ONES;  // rows NG..7 of the zero-point MMA sum p (l)
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
     uint32_t vw[NG];
@@ -416,7 +422,8 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
     float zq[4] = {0.f, 0.f, 0.f, 0.f};
     mma16816_b64(zq, za, zb, 0u, 0u, qf.qz());
     mma16816_b64(zq, za, zb, 0u, 0u, qf.qzlo());
-    float ta0 = zq[0] * qscale, ta1 = zq[1] * qscale, tb0 = zq[2] * qscale, tb1 = zq[3] * qscale;
+    float ta0 = fmaf(zq[0], qscale, -st.m0), ta1 = fmaf(zq[1], qscale, -st.m1);
+    float tb0 = fmaf(zq[2], qscale, -st.m0), tb1 = fmaf(zq[3], qscale, -st.m1);
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
       const float s_a = half_f(pa[j >> 1], j & 1) * fs, s_b = half_f(pb[j >> 1], j & 1) * fs;
@@ -473,8 +480,9 @@ __device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int n
       else return z ? 1 : 0;
     };
     {
-      const uint32_t zab = pair_h(pw(pa, jz, true), pw(pb, jz, true), ph(jz, true));
-      const uint32_t zcd = pair_h(pw(pc, jz, true), pw(pd, jz, true), ph(jz, true));
+      uint32_t zab = pair_h(pw(pa, jz, true), pw(pb, jz, true), ph(jz, true));
+      uint32_t zcd = pair_h(pw(pc, jz, true), pw(pd, jz, true), ph(jz, true));
+      if (g >= NG) zab = zcd = ONES;  // rows NG..7 sum p (l)
       mma16816_b64(acc.zs, zab, zab, zcd, zcd, pack_b64(bP[ks][0], bP[ks][1]));
     }
 #pragma unroll
@@ -610,7 +618,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
   acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
   acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
-  Softmax st{-INFINITY, -INFINITY, 0.f, 0.f};
+  Softmax st{0.f, 0.f, false};
 
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
@@ -638,12 +646,9 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     }
   }
 
-  // ---- finalize this warp: full l per head, acc[h][c] = 2^20 or 2^18 * O^T + zsum ----
-#pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    st.l0 += __shfl_xor_sync(0xffffffffu, st.l0, off);
-    st.l1 += __shfl_xor_sync(0xffffffffu, st.l1, off);
-  }
+  // ---- finalize this warp: l per head from the ones rows, acc[h][c] = 2^(24-2e) O^T + zsum ----
+  const float l0 = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[0], 28 + q);  // row 7 >= NG
+  const float l1 = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[1], 28 + q);
   __syncthreads();  // all warps done with their rings -> reuse ring smem for the merge
   float* sm_acc = reinterpret_cast<float*>(smem);
   float* sm_m = sm_acc + NW * 8 * D;
@@ -667,10 +672,10 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(acc.o[m][3], f1, z1[j]);
   }
   if (g == 0) {
-    sm_m[warp * 8 + 2 * q] = st.m0;
-    sm_m[warp * 8 + 2 * q + 1] = st.m1;
-    sm_l[warp * 8 + 2 * q] = st.l0;
-    sm_l[warp * 8 + 2 * q + 1] = st.l1;
+    sm_m[warp * 8 + 2 * q] = st.init ? st.m0 : -INFINITY;  // a warp without tiles contributes nothing
+    sm_m[warp * 8 + 2 * q + 1] = st.init ? st.m1 : -INFINITY;
+    sm_l[warp * 8 + 2 * q] = l0;
+    sm_l[warp * 8 + 2 * q + 1] = l1;
   }
   finish_piece<D>(a, u, sm_m, sm_l, sm_acc, &sm_flag);
   __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
