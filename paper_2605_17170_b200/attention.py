@@ -28,8 +28,10 @@ from .errors import ValidationError
 from .plan import NUM_SMS_B200, plan_stream
 from .pool import MixedPrecisionPool, PageTable, csr_tables, split_partitioned
 
-VARIANT_TENSOR_CORE = 0
-VARIANT_SIMPLE = 1
+VARIANT_TENSOR_CORE = 0  # warp-specialised QK / PV pairs (8 warps per CTA)
+VARIANT_SIMPLE = 1       # CUDA-core fp32 cross-check
+VARIANT_FUSED = 4        # one warp per tile stream (QK + softmax + PV), 4 warps per CTA
+CTAS_PER_SM = 2          # resident CTAs of the variant-0 kernel (128 regs x 256 threads, ~100 KB smem)
 
 
 @dataclass
@@ -89,7 +91,7 @@ class DecodeBatch:
             n_sm = NUM_SMS_B200
             if pool.device is not None and pool.device.type == "cuda":
                 n_sm = torch.cuda.get_device_properties(pool.device).multi_processor_count
-            kw["n_cta"] = n_sm * int(kw.pop("ctas_per_sm", 3))
+            kw["n_cta"] = n_sm * int(kw.pop("ctas_per_sm", CTAS_PER_SM))
         else:
             kw.pop("ctas_per_sm", None)
         work, cta_ptr, n_parts = plan_stream(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride,
