@@ -123,8 +123,9 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
  *   cta_ptr [n_cta + 1]: CTA i runs pieces cta_ptr[i] .. cta_ptr[i+1] (a byte-balanced share
  *     of the batch, see plan.py); the last CTA to finish a split unit merges its partials.
  *   counters [batch * Hkv] int32, zero before the first launch; every launch leaves them zero.
- *   variant: 0 = tensor-core kernel (mma.sync m16n8k16), 1 = simple CUDA-core kernel,
- *     2 = data movement only, 3 = compute only on stale smem (measurement; output meaningless)
+ *   variant: 0 = tensor-core kernel (mma.sync m16n8k16; plan with 3 CTAs per SM), 1 = simple
+ *     CUDA-core kernel, 2 = data movement only, 3 = compute only on stale smem (measurement;
+ *     output meaningless), 4 = warp-specialised tensor-core kernel (plan with 2 CTAs per SM)
  * Requires n_q_heads % Hkv == 0 and n_q_heads / Hkv <= 8, d in {32, 64, 128}. */
 int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype, const uint8_t* int2_pool,
                        const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,

@@ -35,6 +35,10 @@ namespace kvmix {
 #ifndef KVMIX_SPLIT
 #define KVMIX_SPLIT 0
 #endif
+#ifndef KVMIX_PAIRS
+#define KVMIX_PAIRS 0
+#endif
+constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
 constexpr int NW = 4;                 // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr float LOG2E = 1.4426950408889634f;
@@ -235,6 +239,48 @@ __device__ __forceinline__ void softmax_p(float (&sv)[8], Softmax& st, uint32_t 
   bP[0][1] = movtrans(pack_h2(p[2], p[3]));
   bP[1][0] = movtrans(pack_h2(p[4], p[5]));
   bP[1][1] = movtrans(pack_h2(p[6], p[7]));
+}
+
+// Two tiles' logits at once (one vote, one optional rescale for 64 tokens).
+__device__ __forceinline__ void softmax_p2(float (&sv)[8], float (&sw)[8], Softmax& st, uint32_t (&bP)[2][2],
+                                           uint32_t (&bQ)[2][2], float& al0, float& al1, bool& resc) {
+  float tm0 = fmaxf(fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6])), fmaxf(fmaxf(sw[0], sw[2]), fmaxf(sw[4], sw[6])));
+  float tm1 = fmaxf(fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7])), fmaxf(fmaxf(sw[1], sw[3]), fmaxf(sw[5], sw[7])));
+  resc = __any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK);
+  if (resc) {
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
+      tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
+    }
+    const float sh0 = st.init ? fmaxf(tm0, 0.f) : tm0, sh1 = st.init ? fmaxf(tm1, 0.f) : tm1;
+    al0 = st.init ? fast_exp2(-sh0) : 0.f;
+    al1 = st.init ? fast_exp2(-sh1) : 0.f;
+    st.m0 += sh0;
+    st.m1 += sh1;
+    st.init = true;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      sv[i] -= sh0;
+      sv[i + 1] -= sh1;
+      sw[i] -= sh0;
+      sw[i + 1] -= sh1;
+    }
+  }
+  float p[8], r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    p[i] = fast_exp2(sv[i]);
+    r[i] = fast_exp2(sw[i]);
+  }
+  bP[0][0] = movtrans(pack_h2(p[0], p[1]));
+  bP[0][1] = movtrans(pack_h2(p[2], p[3]));
+  bP[1][0] = movtrans(pack_h2(p[4], p[5]));
+  bP[1][1] = movtrans(pack_h2(p[6], p[7]));
+  bQ[0][0] = movtrans(pack_h2(r[0], r[1]));
+  bQ[0][1] = movtrans(pack_h2(r[2], r[3]));
+  bQ[1][0] = movtrans(pack_h2(r[4], r[5]));
+  bQ[1][1] = movtrans(pack_h2(r[6], r[7]));
 }
 
 template <int D>
@@ -680,7 +726,25 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
 
   // tile metadata: the page id (INT2 tile) or this lane's slot (INT4 tile); loaded one
   // iteration before its copy is issued so the copy never waits on the index load
-  auto load_meta = [&](int k) -> int { return k < nmine ? tile_meta(a, u, u.tlo + warp + k * NW, lane) : 0; };
+  // INT2 page ids come 32 tiles per coalesced load (lane i: this warp's tile 32b + i), the
+  // next batch prefetched; INT4 tiles load their 32 slot ids per tile.  k only increases.
+  int ids_cur = 0, ids_nxt = 0, batch_cur = -2;
+  auto load_ids = [&](int b) -> int {
+    const int kk = 32 * b + lane, t = u.tlo + warp + kk * NW;
+    return (kk < nmine && t < u.npg) ? a.page_ids[u.pg0 + t] : 0;
+  };
+  auto load_meta = [&](int k) -> int {
+    if (k >= nmine) return 0;
+    const int t = u.tlo + warp + k * NW;
+    if (t >= u.npg) return tile_meta(a, u, t, lane);
+    const int b = k >> 5;
+    if (b != batch_cur) {
+      ids_cur = (b == batch_cur + 1) ? ids_nxt : load_ids(b);
+      ids_nxt = load_ids(b + 1);
+      batch_cur = b;
+    }
+    return __shfl_sync(0xffffffffu, ids_cur, k & 31);
+  };
   auto issue = [&](int k, int meta, int s) {
     issue_tile<D>(u, u.tlo + warp + k * NW, meta, ring + s * C::BUF, &bars[warp][s], lane, kv2, kv4);
   };
@@ -691,7 +755,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       if (++s0 == STAGES) s0 = 0;
     }
   }
-  int meta_next = load_meta(STAGES);
+  int meta_next = load_meta(STAGES), meta_next2 = load_meta(STAGES + 1);  // metas run two tiles ahead
 
   // ---- Q fragments (see QFrag): built once per CTA by warp 0 into shared memory ----
   uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + NW * STAGES * C::BUF);
@@ -706,13 +770,38 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
   Softmax st{0.f, 0.f, false};
 
-  for (int k = 0; k < nmine; ++k) {
+  for (int k = 0; k < nmine;) {
     const int t = u.tlo + warp + k * NW;
     const uint8_t* buf = ring + stage * C::BUF;
-    const int meta = meta_next;
-    meta_next = load_meta(k + STAGES + 1);
+    const int stage2 = stage + 1 == STAGES ? 0 : stage + 1;
+    const uint32_t phase2 = stage + 1 == STAGES ? phase ^ 1u : phase;
+    // two same-bitwidth full tiles at once (64 tokens: more independent MMA chains, one vote)
+    const bool two = PAIRS && COMPUTE && k + 1 < nmine &&
+                     ((t + NW < u.npg) || (t >= u.npg && u.n4 - 32 * (t + NW - u.npg) >= 32));
     if (MEMORY) mbar_wait(&bars[warp][stage], phase);
-    if (!COMPUTE) {
+    if (two) {
+      if (MEMORY) mbar_wait(&bars[warp][stage2], phase2);
+      const uint8_t* buf2 = ring + stage2 * C::BUF;
+      float sv[8], sw[8];
+      uint32_t bP[2][2], bQ[2][2];
+      float al0, al1;
+      bool resc;
+      if (t < u.npg) {
+        int2_qk<D, LO>(buf, qf, a.qscale, lane, st, sv);
+        int2_qk<D, LO>(buf2, qf, a.qscale, lane, st, sw);
+        softmax_p2(sv, sw, st, bP, bQ, al0, al1, resc);
+        if (resc) rescale_acc<D>(acc, al0, al1);
+        int2_pv<D>(buf, bP, lane, acc);
+        int2_pv<D>(buf2, bQ, lane, acc);
+      } else {
+        int4_qk<D, true, LO>(buf, 32, qf, a.qscale, lane, st, sv);
+        int4_qk<D, true, LO>(buf2, 32, qf, a.qscale, lane, st, sw);
+        softmax_p2(sv, sw, st, bP, bQ, al0, al1, resc);
+        if (resc) rescale_acc<D>(acc, al0, al1);
+        int4_pv<D, true>(buf, 32, bP, lane, acc);
+        int4_pv<D, true>(buf2, 32, bQ, lane, acc);
+      }
+    } else if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
     } else if (t < u.npg) {
       int2_tile<D, LO>(buf, qf, a.qscale, lane, st, acc);
@@ -722,13 +811,19 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       else int4_tile<D, false, LO>(buf, nv, qf, a.qscale, lane, st, acc);
     }
     __syncwarp();
-    if (MEMORY && k + STAGES < nmine) {
-      fence_proxy_async();
-      issue(k + STAGES, meta, stage);
-    }
-    if (++stage == STAGES) {
-      stage = 0;
-      phase ^= 1u;
+    const int nt = two ? 2 : 1;
+    for (int i = 0; i < nt; ++i) {
+      if (MEMORY && k + STAGES < nmine) {
+        fence_proxy_async();
+        issue(k + STAGES, meta_next, stage);
+      }
+      meta_next = meta_next2;
+      meta_next2 = load_meta(k + STAGES + 2);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      ++k;
     }
   }
 
@@ -752,7 +847,7 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
 }
 
 // ====================================================================================
-// Variant 0: warp-specialised tensor-core kernel.  A CTA holds NPAIR pairs of warps; in
+// Variant 4: warp-specialised tensor-core kernel.  A CTA holds NPAIR pairs of warps; in
 // pair p, warp p (QK) issues the TMA copies of the pair's tiles and computes the logits
 // S = QK^T (dequantised in registers), handing them (32 B per lane) to warp p + NPAIR (PV)
 // through the tile's own ring slot; the PV warp runs the online softmax and owns the
@@ -1006,11 +1101,11 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
   switch (variant) {
     case 0:
       // fp32 q carries bits fp16 cannot hold: add the q - fp16(q) correction MMAs
-      if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_ws_kernel<D, true>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
-      return launch_kernel(decode_ws_kernel<D, false>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
-    case 4:
       if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_mma_kernel<D, true, true, true>, a, n_work, Cfg<D>::SMEM, s);
       return launch_kernel(decode_mma_kernel<D, true, true, false>, a, n_work, Cfg<D>::SMEM, s);
+    case 4:
+      if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_ws_kernel<D, true>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
+      return launch_kernel(decode_ws_kernel<D, false>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
     case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, 0, s);
     case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
     case 3: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);

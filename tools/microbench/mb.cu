@@ -45,7 +45,7 @@ __global__ void ldg_kernel(const int4* __restrict__ p, size_t n, int4* out) {
 
 // one warp per CTA-stage ring; each warp streams 3072-byte chunks via cp.async.bulk
 template <int STAGES, int CHUNK>
-__global__ void bulk_kernel(const uint8_t* __restrict__ p, size_t nchunks, int* out) {
+__global__ void bulk_kernel(const uint8_t* __restrict__ p, size_t nchunks, int* out, int mode = 0) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar[8][STAGES];
   int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -64,7 +64,12 @@ __global__ void bulk_kernel(const uint8_t* __restrict__ p, size_t nchunks, int* 
     int s = k % STAGES;
     uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[warp][s]);
     uint32_t d = (uint32_t)__cvta_generic_to_shared(ring + s * CHUNK);
-    const uint8_t* src = p + (gw + k * nwt) * CHUNK;
+    // mode 0: warps interleaved chunk by chunk; 1: each warp its own contiguous stream;
+    // 2: each CTA a contiguous region, its warps interleaved inside it
+    size_t idx = mode == 0 ? gw + k * nwt
+               : mode == 1 ? gw * mine + k
+               : (size_t)blockIdx.x * nw * mine + k * nw + warp;
+    const uint8_t* src = p + idx * CHUNK;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(CHUNK));
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d), "l"(src), "r"(CHUNK), "r"(b) : "memory");
   };
@@ -129,6 +134,23 @@ int main() {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     printf("LDG.128 stream read: %.1f GB/s\n", bytes / ms / 1e6);
+  }
+  for (int mode : {0, 1, 2}) {
+    constexpr int ST = 2, CH = 3072;
+    int wpb = 4, occ = 3;
+    int smem = wpb * ST * CH;
+    CK(cudaFuncSetAttribute(bulk_kernel<ST, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int blocks = prop.multiProcessorCount * occ;
+    size_t nch = bytes / CH / (blocks * wpb) * (blocks * wpb);
+    bulk_kernel<ST, CH><<<blocks, wpb * 32, smem>>>(buf, nch, (int*)dout, mode);
+    CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    bulk_kernel<ST, CH><<<blocks, wpb * 32, smem>>>(buf, nch, (int*)dout, mode);
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("pattern mode %d (2 stages x 3072 B, 4 warps, 3 blk/SM): %.1f GB/s\n", mode, nch * (double)CH / ms / 1e6);
   }
   {
     constexpr int ST = 4, CH = 3072;
