@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--int4-weight", type=float, default=1.0, help="stream-K planner: cost weight of INT4 bytes")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-k1", action="store_true", help="skip the K1 quantize+pack (cfg3 slice) measurement")
     ap.add_argument("--cpu-sample-units", type=int, default=0, help="(request, layer) units timed on CPU")
     ap.add_argument("--profile-only", action="store_true", help="build + a few steps, no JSON (for ncu)")
     return ap.parse_args()
@@ -298,6 +299,47 @@ def _prefill_layers(pool, table, k, v, l0):
     pool._int4_written[l0:l0 + k.shape[0], :, s[t4] - cfg.offset] = True
 
 
+def measure_k1(args, device, peak) -> dict:
+    """K1 (quantize + pack into the mixed pool, write_prefill's data path) on a cfg3 slice:
+    one 128K-token request whose per-token bits are the concatenated reference-tagged
+    bits of 4 x 32K-token traces, 8 of cfg3's 64 layers, 8 kv heads, d=128, bf16 K/V
+    resident in HBM.  Algorithmic bytes = bf16 K+V in + packed records out."""
+    import torch
+
+    import paper_2605_17170_b200 as kv
+    L, H, d, N = 8, args.kv_heads, args.head_dim, 4 * 32768
+    bits = np.concatenate(tagged_bits(4, 32768, seed_offset=100))
+    g = 32
+    n_pages = int((bits == 2).sum()) // g
+    n4 = N - n_pages * g
+    cfg = kv.PoolConfig(total_slots=N, offset=n_pages * g, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg, device=device)
+    table = pool.alloc("trace", bits)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(7)
+    k = torch.randn((L, N, H, d), device=device, generator=gen).to(torch.bfloat16)
+    v = torch.randn((L, N, H, d), device=device, generator=gen).to(torch.bfloat16)
+    _prefill_layers(pool, table, k, v, 0)  # warm-up (and index upload)
+    torch.cuda.synchronize()
+    reps = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        _prefill_layers(pool, table, k, v, 0)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    bytes_in = 2 * k.numel() * k.element_size()
+    bytes_out = L * H * (n_pages * pool.page_stride + n4 * 2 * kv.token_block_payload_bytes(d, 4))
+    gbs = (bytes_in + bytes_out) / (ms / 1000.0) / 1e9
+    del k, v, pool
+    torch.cuda.empty_cache()
+    return {"workload": "cfg3 slice: 128K-token tagged trace, 8 of 64 layers, 8 kv heads, d=128, bf16 in",
+            "ms_per_call": ms, "ms_per_layer": ms / L, "cfg3_ms_64_layers": ms / L * 64,
+            "bytes_in": bytes_in, "bytes_out": int(bytes_out), "achieved_gbs": gbs, "frac": gbs / peak,
+            "stored_int2_fraction": n_pages * g / N, "note": "index upload (H2D of the page lists) inside the timing"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -437,6 +479,8 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "parity_vs_cuda_core_variant_max_abs": parity,
     }
+    if not args.no_k1:
+        line["k1_prefill"] = measure_k1(args, device, peak)
     if not args.no_cpu_baseline and world == 1:
         workers = os.cpu_count() or 1
         line["cpu_baseline"] = cpu_baseline(args, max(workers, args.cpu_sample_units or workers), workers)

@@ -36,9 +36,10 @@ __device__ __forceinline__ void encode_token_warp(const float (&v)[D / 32], cons
   if (!finite && err) atomicOr(err, 1);
   float scale, zero;
   group_params(mn, mx, LEVELS, scale, zero);
+  const FastQ f = fast_q(scale, zero);
   uint32_t bits = 0;
 #pragma unroll
-  for (int i = 0; i < CPL; ++i) bits |= quant_code(v[i], scale, zero, LEVELS) << (BITS * i);
+  for (int i = 0; i < CPL; ++i) bits |= fast_code(v[i], f, scale, zero, LEVELS) << (BITS * i);
   uint32_t word = bits << (BITS * CPL * (lane % LPW));
 #pragma unroll
   for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
@@ -259,10 +260,77 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t 
 }
 
 // ------------------------------ pool data plane ----------------------------------------
-// write_prefill INT2 branch (pool.py:236-252 -> write_page :201-215): one block per
-// (request page, kv head, layer).  Threads c < D encode the KeyPageBlock column c;
-// the 4 warps encode the page's 32 INT2 V TokenBlocks.  The record is assembled in
-// shared memory in the device layout and leaves with coalesced 16-byte stores.
+// write_prefill INT2 branch (pool.py:236-252 -> write_page :201-215): one CTA per
+// (request page, kv head, layer).  The page's 32 K and V rows are staged in shared memory
+// with 16-byte loads (chunks XOR-swizzled by row), then every thread encodes 64 elements:
+// either one KeyPageBlock channel pair (2 x 32 tokens, quant.py:160-177) or two V
+// TokenBlock groups of consecutive tokens (quant.py:189-232), with the exact-fast code
+// path (FastQ).  The record is assembled in shared memory in the device layout and leaves
+// with coalesced 16-byte stores.
+template <int D, typename T>
+struct PrefillCfg {
+  static constexpr int ROWB = D * (int)sizeof(T);  // bytes per staged token row
+  static constexpr int CHUNKS = ROWB / 16;
+  static constexpr int SWZ = CHUNKS >= 8 ? 7 : CHUNKS - 1;
+  static constexpr int TILE = G * ROWB;
+  static constexpr int SMEM = 2 * TILE + page_stride(D);
+};
+
+template <typename T>
+__device__ __forceinline__ void unpack2(uint32_t w, float& a, float& b);
+template <>
+__device__ __forceinline__ void unpack2<__nv_bfloat16>(uint32_t w, float& a, float& b) {
+  a = __uint_as_float(w << 16);
+  b = __uint_as_float(w & 0xffff0000u);
+}
+template <>
+__device__ __forceinline__ void unpack2<__half>(uint32_t w, float& a, float& b) {
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
+  a = f.x;
+  b = f.y;
+}
+
+template <int D, typename T>
+__device__ __forceinline__ uint8_t* staged(uint8_t* tile, int row, int byte) {
+  using P = PrefillCfg<D, T>;
+  return tile + row * P::ROWB + ((((byte >> 4) ^ ((row >> 1) & P::SWZ))) << 4) + (byte & 15);
+}
+// two consecutive channels (c even) of staged row `row`
+template <int D, typename T>
+__device__ __forceinline__ void load_pair(uint8_t* tile, int row, int c, float& a, float& b) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 v = *reinterpret_cast<const float2*>(staged<D, T>(tile, row, 4 * c));
+    a = v.x;
+    b = v.y;
+  } else {
+    unpack2<T>(*reinterpret_cast<const uint32_t*>(staged<D, T>(tile, row, 2 * c)), a, b);
+  }
+}
+
+// 32 values of one group -> (scale, zero) and 2-bit codes packed in two words (code i at bits 2(i%16))
+__device__ __forceinline__ void encode_group2(const float (&x)[G], uint32_t& w0, uint32_t& w1, uint32_t& pz,
+                                              int32_t* err) {
+  float mn = x[0], mx = x[0];
+  bool finite = true;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    mn = fminf(mn, x[j]);
+    mx = fmaxf(mx, x[j]);
+    finite &= isfinite(x[j]);
+  }
+  if (!finite && err) atomicOr(err, 1);
+  float scale, zero;
+  group_params(mn, mx, 3, scale, zero);
+  const FastQ f = fast_q(scale, zero);
+  w0 = w1 = 0u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    w0 |= fast_code(x[j], f, scale, zero, 3) << (2 * j);
+    w1 |= fast_code(x[j + 16], f, scale, zero, 3) << (2 * j);
+  }
+  pz = pack_param(scale, zero);
+}
+
 template <int D, typename T>
 __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                             int64_t n_tokens, int64_t n_kv_heads,
@@ -270,30 +338,97 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
                                                             const int32_t* __restrict__ page_ids,
                                                             uint8_t* __restrict__ int2_pool, int64_t pool_pages,
                                                             int32_t* err) {
-  const int p = blockIdx.x, h = blockIdx.y, l = blockIdx.z;
+  using P = PrefillCfg<D, T>;
+  extern __shared__ __align__(16) uint8_t psm[];
+  uint8_t* Ks = psm;
+  uint8_t* Vs = psm + P::TILE;
+  uint8_t* srec = psm + 2 * P::TILE;
   __shared__ int tok[G];
-  __shared__ __align__(16) uint8_t srec[page_stride(D)];
-  if (threadIdx.x < G) tok[threadIdx.x] = page_tokens[(int64_t)p * G + threadIdx.x];
+  const int p = blockIdx.x, h = blockIdx.y, l = blockIdx.z, tid = threadIdx.x;
+  if (tid < G) tok[tid] = page_tokens[(int64_t)p * G + tid];
   __syncthreads();
-  const int64_t page = page_ids[p];
-  uint8_t* rec = int2_pool + (((int64_t)l * n_kv_heads + h) * pool_pages + page) * page_stride(D);
-  auto elem = [&](int t, int c) -> int64_t { return (((int64_t)l * n_tokens + t) * n_kv_heads + h) * D + c; };
-  for (int c = threadIdx.x; c < D; c += 128) {
-    float x[G];
-#pragma unroll
-    for (int j = 0; j < G; ++j) x[j] = to_f32(keys[elem(tok[j], c)]);
-    encode_key_channel<D>(x, srec, c, err);
-  }
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  for (int j = warp; j < G; j += 4) {
-    float v[D / 32];
-#pragma unroll
-    for (int i = 0; i < D / 32; ++i) v[i] = to_f32(values[elem(tok[j], lane * (D / 32) + i)]);
-    encode_token_warp<D, 2>(v, PageVStore<D>{srec, j}, lane, err);
+  auto row_ptr = [&](const T* base, int t) {
+    return reinterpret_cast<const uint4*>(base + (((int64_t)l * n_tokens + t) * n_kv_heads + h) * D);
+  };
+  for (int i = tid; i < 2 * G * P::CHUNKS; i += 128) {
+    const int tile = i / (G * P::CHUNKS), r = (i / P::CHUNKS) % G, ch = i % P::CHUNKS;
+    const uint4 v = __ldg(row_ptr(tile ? values : keys, tok[r]) + ch);
+    *reinterpret_cast<uint4*>(staged<D, T>(tile ? Vs : Ks, r, 16 * ch)) = v;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < page_stride(D) / 16; i += 128)
+  for (int it = tid; it < D; it += 128) {
+    if (it < D / 2) {
+      // KeyPageBlock channels c, c+1 over the page's 32 tokens
+      const int c = 2 * it;
+      float xa[G], xb[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) load_pair<D, T>(Ks, j, c, xa[j], xb[j]);
+      uint32_t a0, a1, b0, b1, pa, pb;
+      encode_group2(xa, a0, a1, pa, err);
+      encode_group2(xb, b0, b1, pb, err);
+#pragma unroll
+      for (int tau = 0; tau < 8; ++tau) {  // byte tau of both channel words: adjacent in KC row tau
+        const uint32_t ba = ((tau < 4 ? a0 : a1) >> (8 * (tau & 3))) & 0xffu;
+        const uint32_t bb = ((tau < 4 ? b0 : b1) >> (8 * (tau & 3))) & 0xffu;
+        *reinterpret_cast<uint16_t*>(srec + pg_kc_off(D, tau, c)) = (uint16_t)(ba | (bb << 8));
+      }
+      uint16_t* ks = reinterpret_cast<uint16_t*>(srec + PG_KS(D));
+      uint16_t* kz = reinterpret_cast<uint16_t*>(srec + PG_KZ(D));
+      ks[pg_kp_idx(D, c)] = (uint16_t)(pa & 0xffffu);
+      kz[pg_kp_idx(D, c)] = (uint16_t)(pa >> 16);
+      ks[pg_kp_idx(D, c + 1)] = (uint16_t)(pb & 0xffffu);
+      kz[pg_kp_idx(D, c + 1)] = (uint16_t)(pb >> 16);
+    } else {
+      // V TokenBlock group j of tokens t, t+1 (t even): 2 x 32 channels
+      const int pr = it - D / 2, j = pr / (G / 2), t = 2 * (pr % (G / 2));
+      float xa[G], xb[G];
+#pragma unroll
+      for (int c = 0; c < G; c += 2) {
+        load_pair<D, T>(Vs, t, 32 * j + c, xa[c], xa[c + 1]);
+        load_pair<D, T>(Vs, t + 1, 32 * j + c, xb[c], xb[c + 1]);
+      }
+      uint32_t a0, a1, b0, b1, pa, pb;
+      encode_group2(xa, a0, a1, pa, err);
+      encode_group2(xb, b0, b1, pb, err);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // code byte b = 8j + k of tokens t, t+1: adjacent in their VC word
+        const uint32_t ba = ((k < 4 ? a0 : a1) >> (8 * (k & 3))) & 0xffu;
+        const uint32_t bb = ((k < 4 ? b0 : b1) >> (8 * (k & 3))) & 0xffu;
+        *reinterpret_cast<uint16_t*>(srec + PG_VC(D) + pg_vc_off(D, t, 8 * j + k)) = (uint16_t)(ba | (bb << 8));
+      }
+      uint16_t* vs = reinterpret_cast<uint16_t*>(srec + PG_VS(D));
+      uint16_t* vz = reinterpret_cast<uint16_t*>(srec + PG_VZ(D));
+      vs[pg_vp_idx(D, t, j)] = (uint16_t)(pa & 0xffffu);
+      vz[pg_vp_idx(D, t, j)] = (uint16_t)(pa >> 16);
+      vs[pg_vp_idx(D, t + 1, j)] = (uint16_t)(pb & 0xffffu);
+      vz[pg_vp_idx(D, t + 1, j)] = (uint16_t)(pb >> 16);
+    }
+  }
+  __syncthreads();
+  uint8_t* rec = int2_pool + (((int64_t)l * n_kv_heads + h) * pool_pages + page_ids[p]) * page_stride(D);
+  for (int i = tid; i < page_stride(D) / 16; i += 128)
     reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
+}
+
+// this lane's D/32 consecutive elements, one vector load when they fill 8 or 16 bytes
+template <int D, typename T>
+__device__ __forceinline__ void load_lane(const T* __restrict__ p, float (&v)[D / 32]) {
+  constexpr int NB = (D / 32) * (int)sizeof(T);
+  if constexpr (sizeof(T) == 2 && (NB == 8 || NB == 16)) {
+    uint32_t w[NB / 4];
+    if constexpr (NB == 8) {
+      const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+      w[0] = x.x; w[1] = x.y;
+    } else {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+      w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+    }
+#pragma unroll
+    for (int i = 0; i < NB / 4; ++i) unpack2<T>(w[i], v[2 * i], v[2 * i + 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < D / 32; ++k) v[k] = to_f32(p[k]);
+  }
 }
 
 // INT4 tokens: write_prefill :253-262, write_token :217-226, append_decode_token :284-306.
@@ -322,11 +457,9 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
   uint8_t* rec =
       int4_pool + (((layer0 + l) * n_kv_heads + h) * pool_int4 + (int64_t)int4_ids[i]) * SS;
   float v[D / 32];
-#pragma unroll
-  for (int k = 0; k < D / 32; ++k) v[k] = to_f32(keys[base + k]);
+  load_lane<D, T>(keys + base, v);
   encode_token_warp<D, 4>(v, SlotStore<D, false>{st}, lane, err);
-#pragma unroll
-  for (int k = 0; k < D / 32; ++k) v[k] = to_f32(values[base + k]);
+  load_lane<D, T>(values + base, v);
   encode_token_warp<D, 4>(v, SlotStore<D, true>{st}, lane, err);
   __syncwarp();
   if (lane < SS / 16) reinterpret_cast<uint4*>(rec)[lane] = reinterpret_cast<const uint4*>(st)[lane];
@@ -504,8 +637,14 @@ static int launch_prefill(const void* keys, const void* values, int64_t L, int64
   const T* v = (const T*)values;
   if (np > 0) {
     dim3 grid((unsigned)np, (unsigned)H, (unsigned)L);
-    DISPATCH_D(d, prefill_pages_kernel<D, T><<<grid, 128, 0, s>>>(k, v, N, H, page_tokens, page_ids, int2_pool,
-                                                                  pool_pages, err));
+    DISPATCH_D(d, {
+      constexpr int SM = PrefillCfg<D, T>::SMEM;
+      if (SM > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(prefill_pages_kernel<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+        if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
+      }
+      prefill_pages_kernel<D, T><<<grid, 128, SM, s>>>(k, v, N, H, page_tokens, page_ids, int2_pool, pool_pages, err);
+    });
   }
   if (n4 > 0) {
     dim3 grid((unsigned)((n4 + 3) / 4), (unsigned)H, (unsigned)L);

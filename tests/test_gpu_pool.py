@@ -59,6 +59,47 @@ def test_prefill_bytes_match_oracle(cuda, d, dtype):
     pool.check_invariants()
 
 
+def _near_tie_values(rng, shape, levels):
+    """Groups whose codes sit on or within a few ulps of the round-half-away ties
+    (t = k + 1/2): the fast reciprocal code path must hand these to the exact path."""
+    x = np.empty(shape, np.float32)
+    flat = x.reshape(-1, 32)
+    for gi in range(flat.shape[0]):
+        s = np.float32(2.0 ** rng.integers(-4, 3))
+        a = np.float32(rng.integers(-200, 200)) * s
+        k = rng.integers(0, levels, 32)
+        eps = rng.choice([0.0, 2 ** -23, -(2 ** -23), 2 ** -22, -(2 ** -22), 3e-7, -3e-7], 32)
+        g = (a + (k + 0.5) * s * (1 + eps)).astype(np.float32)
+        g[0], g[1] = a, a + np.float32(levels) * s  # exact min / max -> exact fp16 (scale, zero)
+        flat[gi] = rng.permutation(g)
+    return x
+
+
+def test_prefill_near_ties_bit_exact(cuda):
+    """Bit-exactness where it is hardest: values at and next to the rounding ties, for
+    both the INT2 page path (per-channel keys, per-token values) and the INT4 path."""
+    L, H, d, n = 1, 2, 128, 96
+    rng = np.random.default_rng(11)
+    bits = np.array([2] * 64 + [4] * 32)
+    cfg = kv.PoolConfig(total_slots=256, offset=128, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(256, 128, L, H, d))
+    # keys: ties along tokens within each channel of a page -> build [L, H, d, 32] groups then transpose
+    kp = _near_tie_values(rng, (L, 2, H, d, 32), 3)  # 2 pages
+    k2 = np.moveaxis(kp, 4, 2).reshape(L, 2 * 32, H, d)  # -> [L, tokens, H, d]
+    v2 = _near_tie_values(rng, (L, 64, H, d), 3)
+    k4 = _near_tie_values(rng, (L, 32, H, d), 15)
+    v4 = _near_tie_values(rng, (L, 32, H, d), 15)
+    k = np.concatenate([k2, k4], 1)
+    v = np.concatenate([v2, v4], 1)
+    t = pool.alloc("r", bits)
+    assert t.slots.tolist() == op.alloc("r", bits)
+    pool.write_prefill(t, k, v)
+    op.write_prefill("r", k, v)
+    torch.cuda.synchronize()
+    assert_same_image(pool, op)
+
+
 def test_gather_and_read_slot(cuda):
     L, H, d = 2, 2, 64
     cfg = kv.PoolConfig(total_slots=600, offset=320, n_layers=L, n_kv_heads=H, head_dim=d)
