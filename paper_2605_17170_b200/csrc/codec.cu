@@ -431,10 +431,56 @@ __device__ __forceinline__ void load_lane(const T* __restrict__ p, float (&v)[D 
   }
 }
 
+// 32 values of one group -> (scale, zero) and 4-bit codes packed in four words (code i at bits 4(i%8))
+__device__ __forceinline__ void encode_group4(const float (&x)[G], uint32_t (&w)[4], uint32_t& pz, int32_t* err) {
+  float mn = x[0], mx = x[0];
+  bool finite = true;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    mn = fminf(mn, x[j]);
+    mx = fmaxf(mx, x[j]);
+    finite &= isfinite(x[j]);
+  }
+  if (!finite && err) atomicOr(err, 1);
+  float scale, zero;
+  group_params(mn, mx, 15, scale, zero);
+  const FastQ f = fast_q(scale, zero);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t word = 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) word |= fast_code(x[8 * k + j], f, scale, zero, 15) << (4 * j);
+    w[k] = word;
+  }
+  pz = pack_param(scale, zero);
+}
+
+// 32 consecutive elements -> fp32 (vector loads)
+template <typename T>
+__device__ __forceinline__ void load_group(const T* __restrict__ p, float (&x)[G]) {
+  if constexpr (sizeof(T) == 2) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + i);
+      unpack2<T>(v.x, x[8 * i], x[8 * i + 1]);
+      unpack2<T>(v.y, x[8 * i + 2], x[8 * i + 3]);
+      unpack2<T>(v.z, x[8 * i + 4], x[8 * i + 5]);
+      unpack2<T>(v.w, x[8 * i + 6], x[8 * i + 7]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p) + i);
+      x[4 * i] = v.x; x[4 * i + 1] = v.y; x[4 * i + 2] = v.z; x[4 * i + 3] = v.w;
+    }
+  }
+}
+
 // INT4 tokens: write_prefill :253-262, write_token :217-226, append_decode_token :284-306.
-// Warp per (token, kv head, layer); input element (l, t, h, c) at
-// ((t_stride_l * l) + t * tok_stride + h * D + c) with explicit strides.  The slot
-// record is staged per warp in shared memory (device layout) and stored as 16 B words.
+// A warp encodes 32 / (D/32) tokens of one (kv head, layer): lane = (token, channel group)
+// quantizes that group of both K and V (64 elements, exact-fast codes, no shuffles).
+// Input element (l, t, h, c) at (l * layer_stride + t * tok_stride + h * D + c); the
+// warp's slot records are staged in shared memory (device layout) and stored as 16 B words.
 template <int D, typename T>
 __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                           int64_t n, int64_t layer_stride, int64_t tok_stride,
@@ -443,26 +489,47 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
                                                           const int32_t* __restrict__ int4_ids,
                                                           uint8_t* __restrict__ int4_pool, int64_t pool_int4,
                                                           int32_t* err) {
-  constexpr int SS = slot_stride(D);
-  __shared__ __align__(16) uint8_t srec[4][SS];
+  constexpr int SS = slot_stride(D), NG = D / 32, TPW = 32 / NG;  // tokens per warp
+  __shared__ __align__(16) uint8_t srec[4][TPW * SS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x / 32;
-  const int64_t i = (int64_t)blockIdx.x * 4 + warp;
   const int h = blockIdx.y, l = blockIdx.z;
-  if (i >= n) return;
+  const int64_t i0 = ((int64_t)blockIdx.x * 4 + warp) * TPW;  // first token index of this warp
+  if (i0 >= n) return;
   uint8_t* st = srec[warp];
-  for (int k = lane; k < SS / 4; k += 32) reinterpret_cast<uint32_t*>(st)[k] = 0u;  // padding stays zero
+  for (int k = lane; k < TPW * SS / 4; k += 32) reinterpret_cast<uint32_t*>(st)[k] = 0u;  // padding stays zero
   __syncwarp();
-  const int64_t t = tokens ? tokens[i] : i;
-  const int64_t base = l * layer_stride + t * tok_stride + (int64_t)h * D + lane * (D / 32);
-  uint8_t* rec =
-      int4_pool + (((layer0 + l) * n_kv_heads + h) * pool_int4 + (int64_t)int4_ids[i]) * SS;
-  float v[D / 32];
-  load_lane<D, T>(keys + base, v);
-  encode_token_warp<D, 4>(v, SlotStore<D, false>{st}, lane, err);
-  load_lane<D, T>(values + base, v);
-  encode_token_warp<D, 4>(v, SlotStore<D, true>{st}, lane, err);
+  const int tw = lane / NG, j = lane % NG;
+  const int64_t i = i0 + tw;
+  if (i < n) {
+    const int64_t t = tokens ? tokens[i] : i;
+    const int64_t base = l * layer_stride + t * tok_stride + (int64_t)h * D + 32 * j;
+    uint8_t* rec = st + tw * SS;
+    float x[G];
+    uint32_t w[4], pz;
+    load_group<T>(keys + base, x);
+    encode_group4(x, w, pz, err);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)  // payload bytes 16j + 4q .. +3 -> record (D/8) q + 4j
+      *reinterpret_cast<uint32_t*>(rec + sl_kc_off(D, 16 * j + 4 * q)) = w[q];
+    reinterpret_cast<uint16_t*>(rec + SL_KS(D))[j] = (uint16_t)(pz & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + SL_KZ(D))[j] = (uint16_t)(pz >> 16);
+    load_group<T>(values + base, x);
+    encode_group4(x, w, pz, err);
+#pragma unroll
+    for (int g = 0; g < 8; ++g)  // payload bytes 16j + 2g, +1 -> record VC + (D/16) g + 2j
+      *reinterpret_cast<uint16_t*>(rec + SL_VC(D) + sl_vc_off(D, 16 * j + 2 * g)) =
+          (uint16_t)((w[g >> 1] >> (16 * (g & 1))) & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + SL_VS(D))[j] = (uint16_t)(pz & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + SL_VZ(D))[j] = (uint16_t)(pz >> 16);
+  }
   __syncwarp();
-  if (lane < SS / 16) reinterpret_cast<uint4*>(rec)[lane] = reinterpret_cast<const uint4*>(st)[lane];
+  const int nt = (int)min((int64_t)TPW, n - i0);
+  for (int c = lane; c < nt * (SS / 16); c += 32) {
+    const int tw2 = c / (SS / 16), k = c % (SS / 16);
+    const int64_t slot = int4_ids[i0 + tw2];
+    reinterpret_cast<uint4*>(int4_pool + (((layer0 + l) * n_kv_heads + h) * pool_int4 + slot) * SS)[k] =
+        reinterpret_cast<const uint4*>(st + tw2 * SS)[k];
+  }
 }
 
 // K5 gather-dequant (pool.py:394-439): thread per (slot, head, channel) -> f32 k/v.
@@ -647,7 +714,8 @@ static int launch_prefill(const void* keys, const void* values, int64_t L, int64
     });
   }
   if (n4 > 0) {
-    dim3 grid((unsigned)((n4 + 3) / 4), (unsigned)H, (unsigned)L);
+    const int64_t tpc = 4 * (32 / (d / 32));  // tokens per CTA
+    dim3 grid((unsigned)((n4 + tpc - 1) / tpc), (unsigned)H, (unsigned)L);
     DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>(k, v, n4, N * H * D, H * D, H, 0, int4_tokens,
                                                                 int4_ids, int4_pool, pool_int4, err));
   }
@@ -680,7 +748,8 @@ template <typename T>
 static int launch_append(const void* k, const void* v, int64_t n, int64_t Lin, int64_t layer0, int64_t H, int64_t d,
                          const int32_t* int4_ids, uint8_t* int4_pool, int64_t pool_int4, int32_t* err,
                          cudaStream_t s) {
-  dim3 grid((unsigned)((n + 3) / 4), (unsigned)H, (unsigned)Lin);
+  const int64_t tpc = 4 * (32 / (d / 32));  // tokens per CTA
+  dim3 grid((unsigned)((n + tpc - 1) / tpc), (unsigned)H, (unsigned)Lin);
   DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>((const T*)k, (const T*)v, n, H * D, Lin * H * D, H,
                                                               layer0, nullptr, int4_ids, int4_pool, pool_int4, err));
   return check_launch("append_int4");
