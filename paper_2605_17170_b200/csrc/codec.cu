@@ -3,6 +3,8 @@
 // every op in the group arithmetic is an explicit round-to-nearest intrinsic
 // (__fsub_rn / __fdiv_rn / __fadd_rn / __float2half_rn), so no contraction or
 // fast-math can change a code, scale or zero.
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -273,7 +275,7 @@ struct PrefillCfg {
   static constexpr int CHUNKS = ROWB / 16;
   static constexpr int SWZ = CHUNKS >= 8 ? 7 : CHUNKS - 1;
   static constexpr int TILE = G * ROWB;
-  static constexpr int SMEM = 2 * TILE + page_stride(D);
+  static constexpr int SMEM = 4 * TILE + page_stride(D);  // 2 stages x (K, V) + the record
 };
 
 template <typename T>
@@ -293,7 +295,12 @@ __device__ __forceinline__ void unpack2<__half>(uint32_t w, float& a, float& b) 
 template <int D, typename T>
 __device__ __forceinline__ uint8_t* staged(uint8_t* tile, int row, int byte) {
   using P = PrefillCfg<D, T>;
-  return tile + row * P::ROWB + ((((byte >> 4) ^ ((row >> 1) & P::SWZ))) << 4) + (byte & 15);
+  return tile + row * P::ROWB + ((((byte >> 4) ^ (row & P::SWZ))) << 4) + (byte & 15);
+}
+// channel c of staged row `row`
+template <int D, typename T>
+__device__ __forceinline__ float load_one(uint8_t* tile, int row, int c) {
+  return to_f32(*reinterpret_cast<const T*>(staged<D, T>(tile, row, (int)sizeof(T) * c)));
 }
 // two consecutive channels (c even) of staged row `row`
 template <int D, typename T>
@@ -333,81 +340,67 @@ __device__ __forceinline__ void encode_group2(const float (&x)[G], uint32_t& w0,
 
 template <int D, typename T>
 __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
-                                                            int64_t n_tokens, int64_t n_kv_heads,
-                                                            const int32_t* __restrict__ page_tokens,
+                                                            int64_t n_tokens, int64_t n_kv_heads, int64_t n_pages,
+                                                            int64_t n_items, const int32_t* __restrict__ page_tokens,
                                                             const int32_t* __restrict__ page_ids,
                                                             uint8_t* __restrict__ int2_pool, int64_t pool_pages,
                                                             int32_t* err) {
+  // Persistent: CTA b runs items b, b + grid, ... (item = (layer, kv head, page)); the K / V
+  // tiles of the next item stream in (cp.async, 2 stages) while this one is encoded.
   using P = PrefillCfg<D, T>;
   extern __shared__ __align__(16) uint8_t psm[];
-  uint8_t* Ks = psm;
-  uint8_t* Vs = psm + P::TILE;
-  uint8_t* srec = psm + 2 * P::TILE;
-  __shared__ int tok[G];
-  const int p = blockIdx.x, h = blockIdx.y, l = blockIdx.z, tid = threadIdx.x;
-  if (tid < G) tok[tid] = page_tokens[(int64_t)p * G + tid];
-  __syncthreads();
-  auto row_ptr = [&](const T* base, int t) {
-    return reinterpret_cast<const uint4*>(base + (((int64_t)l * n_tokens + t) * n_kv_heads + h) * D);
-  };
-  for (int i = tid; i < 2 * G * P::CHUNKS; i += 128) {
-    const int tile = i / (G * P::CHUNKS), r = (i / P::CHUNKS) % G, ch = i % P::CHUNKS;
-    const uint4 v = __ldg(row_ptr(tile ? values : keys, tok[r]) + ch);
-    *reinterpret_cast<uint4*>(staged<D, T>(tile ? Vs : Ks, r, 16 * ch)) = v;
-  }
-  __syncthreads();
-  for (int it = tid; it < D; it += 128) {
-    if (it < D / 2) {
-      // KeyPageBlock channels c, c+1 over the page's 32 tokens
-      const int c = 2 * it;
-      float xa[G], xb[G];
-#pragma unroll
-      for (int j = 0; j < G; ++j) load_pair<D, T>(Ks, j, c, xa[j], xb[j]);
-      uint32_t a0, a1, b0, b1, pa, pb;
-      encode_group2(xa, a0, a1, pa, err);
-      encode_group2(xb, b0, b1, pb, err);
-#pragma unroll
-      for (int tau = 0; tau < 8; ++tau) {  // byte tau of both channel words: adjacent in KC row tau
-        const uint32_t ba = ((tau < 4 ? a0 : a1) >> (8 * (tau & 3))) & 0xffu;
-        const uint32_t bb = ((tau < 4 ? b0 : b1) >> (8 * (tau & 3))) & 0xffu;
-        *reinterpret_cast<uint16_t*>(srec + pg_kc_off(D, tau, c)) = (uint16_t)(ba | (bb << 8));
-      }
-      uint16_t* ks = reinterpret_cast<uint16_t*>(srec + PG_KS(D));
-      uint16_t* kz = reinterpret_cast<uint16_t*>(srec + PG_KZ(D));
-      ks[pg_kp_idx(D, c)] = (uint16_t)(pa & 0xffffu);
-      kz[pg_kp_idx(D, c)] = (uint16_t)(pa >> 16);
-      ks[pg_kp_idx(D, c + 1)] = (uint16_t)(pb & 0xffffu);
-      kz[pg_kp_idx(D, c + 1)] = (uint16_t)(pb >> 16);
-    } else {
-      // V TokenBlock group j of tokens t, t+1 (t even): 2 x 32 channels
-      const int pr = it - D / 2, j = pr / (G / 2), t = 2 * (pr % (G / 2));
-      float xa[G], xb[G];
-#pragma unroll
-      for (int c = 0; c < G; c += 2) {
-        load_pair<D, T>(Vs, t, 32 * j + c, xa[c], xa[c + 1]);
-        load_pair<D, T>(Vs, t + 1, 32 * j + c, xb[c], xb[c + 1]);
-      }
-      uint32_t a0, a1, b0, b1, pa, pb;
-      encode_group2(xa, a0, a1, pa, err);
-      encode_group2(xb, b0, b1, pb, err);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {  // code byte b = 8j + k of tokens t, t+1: adjacent in their VC word
-        const uint32_t ba = ((k < 4 ? a0 : a1) >> (8 * (k & 3))) & 0xffu;
-        const uint32_t bb = ((k < 4 ? b0 : b1) >> (8 * (k & 3))) & 0xffu;
-        *reinterpret_cast<uint16_t*>(srec + PG_VC(D) + pg_vc_off(D, t, 8 * j + k)) = (uint16_t)(ba | (bb << 8));
-      }
-      uint16_t* vs = reinterpret_cast<uint16_t*>(srec + PG_VS(D));
-      uint16_t* vz = reinterpret_cast<uint16_t*>(srec + PG_VZ(D));
-      vs[pg_vp_idx(D, t, j)] = (uint16_t)(pa & 0xffffu);
-      vz[pg_vp_idx(D, t, j)] = (uint16_t)(pa >> 16);
-      vs[pg_vp_idx(D, t + 1, j)] = (uint16_t)(pb & 0xffffu);
-      vz[pg_vp_idx(D, t + 1, j)] = (uint16_t)(pb >> 16);
+  uint8_t* srec = psm + 4 * P::TILE;
+  const int tid = threadIdx.x;
+  auto fetch = [&](int64_t item, int stg) {  // issue the item's 2 x 32 rows into stage stg
+    const int64_t p = item % n_pages, lh = item / n_pages;
+    const int64_t l = lh / n_kv_heads, h = lh % n_kv_heads;
+    uint8_t* Ks = psm + 2 * stg * P::TILE;
+    for (int i = tid; i < 2 * G * P::CHUNKS; i += 128) {
+      const int tile = i / (G * P::CHUNKS), r = (i / P::CHUNKS) % G, ch = i % P::CHUNKS;
+      const int t = page_tokens[p * G + r];
+      const T* src = (tile ? values : keys) + ((l * n_tokens + t) * n_kv_heads + h) * D;
+      cp_async16(staged<D, T>(Ks + tile * P::TILE, r, 16 * ch), reinterpret_cast<const uint4*>(src) + ch);
     }
+  };
+  int stg = 0;
+  if (blockIdx.x < n_items) fetch(blockIdx.x, 0);
+  cp_async_commit();
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, stg ^= 1) {
+    if (item + gridDim.x < n_items) fetch(item + gridDim.x, stg ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();  // this item's tiles have landed (the next item's may still fly)
+    __syncthreads();
+    uint8_t* Ks = psm + 2 * stg * P::TILE;
+    uint8_t* Vs = Ks + P::TILE;
+    // 2D units of 32 values: unit u < D is KeyPageBlock channel u over the 32 tokens, unit
+    // D + 32 j + t is V TokenBlock group j of token t.  One (not unrolled) loop around one
+    // inlined encoder keeps the kernel small enough for the instruction cache.
+#pragma unroll 1
+    for (int u = tid; u < 2 * D; u += 128) {
+      const bool isk = u < D;
+      const int c = u, j = (u - D) / G, t = (u - D) % G;
+      float x[G];
+#pragma unroll
+      for (int i = 0; i < G; ++i) x[i] = isk ? load_one<D, T>(Ks, i, c) : load_one<D, T>(Vs, t, G * j + i);
+      uint32_t w0, w1, pz;
+      encode_group2(x, w0, w1, pz, err);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // code byte b: KC row b of channel c / V code byte 8j + b of token t
+        const int pos = isk ? pg_kc_off(D, b, c) : PG_VC(D) + pg_vc_off(D, t, 8 * j + b);
+        srec[pos] = (uint8_t)(((b < 4 ? w0 : w1) >> (8 * (b & 3))) & 0xffu);
+      }
+      const int pidx = isk ? pg_kp_idx(D, c) : pg_vp_idx(D, t, j);
+      reinterpret_cast<uint16_t*>(srec + (isk ? PG_KS(D) : PG_VS(D)))[pidx] = (uint16_t)(pz & 0xffffu);
+      reinterpret_cast<uint16_t*>(srec + (isk ? PG_KZ(D) : PG_VZ(D)))[pidx] = (uint16_t)(pz >> 16);
+    }
+    __syncthreads();
+    const int64_t p = item % n_pages, lh = item / n_pages;
+    uint8_t* rec = int2_pool + (lh * pool_pages + page_ids[p]) * page_stride(D);
+    for (int i = tid; i < page_stride(D) / 16; i += 128)
+      reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
+    __syncthreads();  // srec and this stage are free
   }
-  __syncthreads();
-  uint8_t* rec = int2_pool + (((int64_t)l * n_kv_heads + h) * pool_pages + page_ids[p]) * page_stride(D);
-  for (int i = tid; i < page_stride(D) / 16; i += 128)
-    reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
+  cp_async_wait<0>();
 }
 
 // this lane's D/32 consecutive elements, one vector load when they fill 8 or 16 bytes
@@ -703,14 +696,21 @@ static int launch_prefill(const void* keys, const void* values, int64_t L, int64
   const T* k = (const T*)keys;
   const T* v = (const T*)values;
   if (np > 0) {
-    dim3 grid((unsigned)np, (unsigned)H, (unsigned)L);
+    const int64_t items = np * H * L;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     DISPATCH_D(d, {
       constexpr int SM = PrefillCfg<D, T>::SMEM;
       if (SM > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(prefill_pages_kernel<D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
         if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
       }
-      prefill_pages_kernel<D, T><<<grid, 128, SM, s>>>(k, v, N, H, page_tokens, page_ids, int2_pool, pool_pages, err);
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prefill_pages_kernel<D, T>, 128, SM);
+      const int64_t grid = std::min<int64_t>(items, (int64_t)n_sm * std::max(per_sm, 1));
+      prefill_pages_kernel<D, T><<<(unsigned)grid, 128, SM, s>>>(k, v, N, H, np, items, page_tokens, page_ids,
+                                                               int2_pool, pool_pages, err);
     });
   }
   if (n4 > 0) {
