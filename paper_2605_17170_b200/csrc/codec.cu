@@ -314,9 +314,11 @@ __device__ __forceinline__ void load_pair(uint8_t* tile, int row, int c, float& 
   }
 }
 
-// 32 values of one group -> (scale, zero) and 2-bit codes packed in two words (code i at bits 2(i%16))
-__device__ __forceinline__ void encode_group2(const float (&x)[G], uint32_t& w0, uint32_t& w1, uint32_t& pz,
-                                              int32_t* err) {
+// 32 values of one group -> (scale, zero) and BITS-bit codes packed in BITS words (code i at
+// bits BITS * (i % (32 / BITS)) of word i / (32 / BITS)), bit-exact with quant.py:36-50.
+template <int BITS>
+__device__ __forceinline__ void encode_group(const float (&x)[G], uint32_t (&w)[BITS], uint32_t& pz, int32_t* err) {
+  constexpr int LEVELS = (1 << BITS) - 1, PER = 32 / BITS;
   float mn = x[0], mx = x[0];
   bool finite = true;
 #pragma unroll
@@ -327,13 +329,39 @@ __device__ __forceinline__ void encode_group2(const float (&x)[G], uint32_t& w0,
   }
   if (!finite && err) atomicOr(err, 1);
   float scale, zero;
-  group_params(mn, mx, 3, scale, zero);
-  const FastQ f = fast_q(scale, zero);
-  w0 = w1 = 0u;
+  group_params(mn, mx, LEVELS, scale, zero);
+  // t = fl(fl(x - zero) / scale), the reference's IEEE quotient, without a division per
+  // element: y = RN(1/scale) once per group, q = RN(d y), e = d - q scale (exact, FMA),
+  // t = RN(q + e y) (Markstein's refinement; the divisor is an fp16 value, never an
+  // all-ones fp32 significand).  tools/microbench/divcheck.cu compares it with __fdiv_rn
+  // for every positive finite fp16 divisor (4.9e9 quotients): every |t| >= 0.25 matches
+  // bit for bit; the only differences are tiny quotients (underflowing residual), whose
+  // code is 0 either way.  Non-finite parameters take quant_code.
+  const bool exact = !(isfinite(scale) && isfinite(zero));
+  const float y = scale > 0.f ? __frcp_rn(scale) : 0.f;
+  constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23: MAGIC + k holds the integer k in its low bits
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    w0 |= fast_code(x[j], f, scale, zero, 3) << (2 * j);
-    w1 |= fast_code(x[j + 16], f, scale, zero, 3) << (2 * j);
+  for (int k = 0; k < BITS; ++k) {
+    uint32_t word = 0u;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const float d = __fsub_rn(x[PER * k + i], zero);
+      const float q = __fmul_rn(d, y);
+      const float t = __fmaf_rn(__fmaf_rn(-q, scale, d), y, q);
+      // round half away, then clip to [0, L] (negative t always gives 0)
+      const float c = fminf(fmaxf(floorf(__fadd_rn(t, 0.5f)), 0.f), (float)LEVELS);
+      word |= (__float_as_uint(__fadd_rn(c, MAGIC)) - 0x4B400000u) << (BITS * i);
+    }
+    w[k] = word;
+  }
+  if (exact) {  // rare (inf / nan parameters): the reference arithmetic verbatim; cold, unrolled
+#pragma unroll
+    for (int k = 0; k < BITS; ++k) {
+      uint32_t word = 0u;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) word |= quant_code_slow(x[PER * k + i], scale, zero, LEVELS) << (BITS * i);
+      w[k] = word;
+    }
   }
   pz = pack_param(scale, zero);
 }
@@ -372,26 +400,33 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     __syncthreads();
     uint8_t* Ks = psm + 2 * stg * P::TILE;
     uint8_t* Vs = Ks + P::TILE;
-    // 2D units of 32 values: unit u < D is KeyPageBlock channel u over the 32 tokens, unit
-    // D + 32 j + t is V TokenBlock group j of token t.  One (not unrolled) loop around one
-    // inlined encoder keeps the kernel small enough for the instruction cache.
+    // KeyPageBlock channel c over the page's 32 tokens (threads 0..D-1) and V TokenBlock
+    // group j of token t (units D + 32 j + t); loops, not unrolled, around one encoder each.
 #pragma unroll 1
-    for (int u = tid; u < 2 * D; u += 128) {
-      const bool isk = u < D;
-      const int c = u, j = (u - D) / G, t = (u - D) % G;
+    for (int c = tid; c < D; c += 128) {
       float x[G];
 #pragma unroll
-      for (int i = 0; i < G; ++i) x[i] = isk ? load_one<D, T>(Ks, i, c) : load_one<D, T>(Vs, t, G * j + i);
-      uint32_t w0, w1, pz;
-      encode_group2(x, w0, w1, pz, err);
+      for (int i = 0; i < G; ++i) x[i] = load_one<D, T>(Ks, i, c);
+      uint32_t w[2], pz;
+      encode_group<2>(x, w, pz, err);
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {  // code byte b: KC row b of channel c / V code byte 8j + b of token t
-        const int pos = isk ? pg_kc_off(D, b, c) : PG_VC(D) + pg_vc_off(D, t, 8 * j + b);
-        srec[pos] = (uint8_t)(((b < 4 ? w0 : w1) >> (8 * (b & 3))) & 0xffu);
-      }
-      const int pidx = isk ? pg_kp_idx(D, c) : pg_vp_idx(D, t, j);
-      reinterpret_cast<uint16_t*>(srec + (isk ? PG_KS(D) : PG_VS(D)))[pidx] = (uint16_t)(pz & 0xffffu);
-      reinterpret_cast<uint16_t*>(srec + (isk ? PG_KZ(D) : PG_VZ(D)))[pidx] = (uint16_t)(pz >> 16);
+      for (int b = 0; b < 8; ++b) srec[pg_kc_off(D, b, c)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
+      reinterpret_cast<uint16_t*>(srec + PG_KS(D))[pg_kp_idx(D, c)] = (uint16_t)(pz & 0xffffu);
+      reinterpret_cast<uint16_t*>(srec + PG_KZ(D))[pg_kp_idx(D, c)] = (uint16_t)(pz >> 16);
+    }
+#pragma unroll 1
+    for (int v = (tid + 128 - D % 128) % 128; v < G * (D / G); v += 128) {
+      const int j = v / G, t = v % G;
+      float x[G];
+#pragma unroll
+      for (int i = 0; i < G; i += 2) load_pair<D, T>(Vs, t, G * j + i, x[i], x[i + 1]);
+      uint32_t w[2], pz;
+      encode_group<2>(x, w, pz, err);
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        srec[PG_VC(D) + pg_vc_off(D, t, 8 * j + b)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
+      reinterpret_cast<uint16_t*>(srec + PG_VS(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz & 0xffffu);
+      reinterpret_cast<uint16_t*>(srec + PG_VZ(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz >> 16);
     }
     __syncthreads();
     const int64_t p = item % n_pages, lh = item / n_pages;
@@ -422,30 +457,6 @@ __device__ __forceinline__ void load_lane(const T* __restrict__ p, float (&v)[D 
 #pragma unroll
     for (int k = 0; k < D / 32; ++k) v[k] = to_f32(p[k]);
   }
-}
-
-// 32 values of one group -> (scale, zero) and 4-bit codes packed in four words (code i at bits 4(i%8))
-__device__ __forceinline__ void encode_group4(const float (&x)[G], uint32_t (&w)[4], uint32_t& pz, int32_t* err) {
-  float mn = x[0], mx = x[0];
-  bool finite = true;
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    mn = fminf(mn, x[j]);
-    mx = fmaxf(mx, x[j]);
-    finite &= isfinite(x[j]);
-  }
-  if (!finite && err) atomicOr(err, 1);
-  float scale, zero;
-  group_params(mn, mx, 15, scale, zero);
-  const FastQ f = fast_q(scale, zero);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t word = 0u;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) word |= fast_code(x[8 * k + j], f, scale, zero, 15) << (4 * j);
-    w[k] = word;
-  }
-  pz = pack_param(scale, zero);
 }
 
 // 32 consecutive elements -> fp32 (vector loads)
@@ -500,14 +511,14 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
     float x[G];
     uint32_t w[4], pz;
     load_group<T>(keys + base, x);
-    encode_group4(x, w, pz, err);
+    encode_group<4>(x, w, pz, err);
 #pragma unroll
     for (int q = 0; q < 4; ++q)  // payload bytes 16j + 4q .. +3 -> record (D/8) q + 4j
       *reinterpret_cast<uint32_t*>(rec + sl_kc_off(D, 16 * j + 4 * q)) = w[q];
     reinterpret_cast<uint16_t*>(rec + SL_KS(D))[j] = (uint16_t)(pz & 0xffffu);
     reinterpret_cast<uint16_t*>(rec + SL_KZ(D))[j] = (uint16_t)(pz >> 16);
     load_group<T>(values + base, x);
-    encode_group4(x, w, pz, err);
+    encode_group<4>(x, w, pz, err);
 #pragma unroll
     for (int g = 0; g < 8; ++g)  // payload bytes 16j + 2g, +1 -> record VC + (D/16) g + 2j
       *reinterpret_cast<uint16_t*>(rec + SL_VC(D) + sl_vc_off(D, 16 * j + 2 * g)) =
