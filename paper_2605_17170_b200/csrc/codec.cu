@@ -297,6 +297,24 @@ __device__ __forceinline__ uint8_t* staged(uint8_t* tile, int row, int byte) {
   using P = PrefillCfg<D, T>;
   return tile + row * P::ROWB + ((((byte >> 4) ^ (row & P::SWZ))) << 4) + (byte & 15);
 }
+// the 32 channels of group j in staged row `row`, as 16-byte loads
+template <int D, typename T>
+__device__ __forceinline__ void load_row_group(uint8_t* tile, int row, int j, float (&x)[G]) {
+  constexpr int PER16 = 16 / (int)sizeof(T);  // elements per 16-byte chunk
+#pragma unroll
+  for (int k = 0; k < G / PER16; ++k) {
+    const uint4 v = *reinterpret_cast<const uint4*>(staged<D, T>(tile, row, (int)sizeof(T) * (G * j + PER16 * k)));
+    if constexpr (sizeof(T) == 4) {
+      x[4 * k] = __uint_as_float(v.x); x[4 * k + 1] = __uint_as_float(v.y);
+      x[4 * k + 2] = __uint_as_float(v.z); x[4 * k + 3] = __uint_as_float(v.w);
+    } else {
+      unpack2<T>(v.x, x[8 * k], x[8 * k + 1]);
+      unpack2<T>(v.y, x[8 * k + 2], x[8 * k + 3]);
+      unpack2<T>(v.z, x[8 * k + 4], x[8 * k + 5]);
+      unpack2<T>(v.w, x[8 * k + 6], x[8 * k + 7]);
+    }
+  }
+}
 // channel c of staged row `row`
 template <int D, typename T>
 __device__ __forceinline__ float load_one(uint8_t* tile, int row, int c) {
@@ -316,18 +334,28 @@ __device__ __forceinline__ void load_pair(uint8_t* tile, int row, int c, float& 
 
 // 32 values of one group -> (scale, zero) and BITS-bit codes packed in BITS words (code i at
 // bits BITS * (i % (32 / BITS)) of word i / (32 / BITS)), bit-exact with quant.py:36-50.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 template <int BITS>
 __device__ __forceinline__ void encode_group(const float (&x)[G], uint32_t (&w)[BITS], uint32_t& pz, int32_t* err) {
   constexpr int LEVELS = (1 << BITS) - 1, PER = 32 / BITS;
+  // NaN-propagating min / max: one finiteness test per group covers every element
   float mn = x[0], mx = x[0];
-  bool finite = true;
 #pragma unroll
-  for (int j = 0; j < G; ++j) {
-    mn = fminf(mn, x[j]);
-    mx = fmaxf(mx, x[j]);
-    finite &= isfinite(x[j]);
+  for (int j = 1; j < G; ++j) {
+    mn = fmin_nan(mn, x[j]);
+    mx = fmax_nan(mx, x[j]);
   }
-  if (!finite && err) atomicOr(err, 1);
+  if (!(isfinite(mn) && isfinite(mx)) && err) atomicOr(err, 1);
   float scale, zero;
   group_params(mn, mx, LEVELS, scale, zero);
   // t = fl(fl(x - zero) / scale), the reference's IEEE quotient, without a division per
@@ -339,7 +367,7 @@ __device__ __forceinline__ void encode_group(const float (&x)[G], uint32_t (&w)[
   // code is 0 either way.  Non-finite parameters take quant_code.
   const bool exact = !(isfinite(scale) && isfinite(zero));
   const float y = scale > 0.f ? __frcp_rn(scale) : 0.f;
-  constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23: MAGIC + k holds the integer k in its low bits
+  constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23: MAGIC + k holds the integer k (< 2^22) in its low bits
 #pragma unroll
   for (int k = 0; k < BITS; ++k) {
     uint32_t word = 0u;
@@ -348,9 +376,10 @@ __device__ __forceinline__ void encode_group(const float (&x)[G], uint32_t (&w)[
       const float d = __fsub_rn(x[PER * k + i], zero);
       const float q = __fmul_rn(d, y);
       const float t = __fmaf_rn(__fmaf_rn(-q, scale, d), y, q);
-      // round half away, then clip to [0, L] (negative t always gives 0)
-      const float c = fminf(fmaxf(floorf(__fadd_rn(t, 0.5f)), 0.f), (float)LEVELS);
-      word |= (__float_as_uint(__fadd_rn(c, MAGIC)) - 0x4B400000u) << (BITS * i);
+      // clip(round_half_away(t), 0, L) == floor(fl(clip(t, 0, L) + 1/2)); the floor comes
+      // from a round-down add of MAGIC, leaving the code in the low mantissa bits
+      const float a = __fadd_rn(fminf(fmaxf(t, 0.f), (float)LEVELS), 0.5f);
+      word |= (__float_as_uint(__fadd_rd(a, MAGIC)) & (uint32_t)LEVELS) << (BITS * i);
     }
     w[k] = word;
   }
@@ -418,8 +447,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     for (int v = (tid + 128 - D % 128) % 128; v < G * (D / G); v += 128) {
       const int j = v / G, t = v % G;
       float x[G];
-#pragma unroll
-      for (int i = 0; i < G; i += 2) load_pair<D, T>(Vs, t, G * j + i, x[i], x[i + 1]);
+      load_row_group<D, T>(Vs, t, j, x);  // 16-byte loads; rows t % 8 of a quarter warp differ: no conflicts
       uint32_t w[2], pz;
       encode_group<2>(x, w, pz, err);
 #pragma unroll
