@@ -368,20 +368,38 @@ __device__ __forceinline__ void encode_group(const float (&x)[G], uint32_t (&w)[
   const bool exact = !(isfinite(scale) && isfinite(zero));
   const float y = scale > 0.f ? __frcp_rn(scale) : 0.f;
   constexpr float MAGIC = 12582912.f;  // 1.5 * 2^23: MAGIC + k holds the integer k (< 2^22) in its low bits
+  auto quot = [&](float v) {
+    const float d = __fsub_rn(v, zero);
+    const float q = __fmul_rn(d, y);
+    return __fmaf_rn(__fmaf_rn(-q, scale, d), y, q);
+  };
+  // clip(round_half_away(t), 0, L) == floor(fl(clip(t, 0, L) + 1/2)); the floor comes from a
+  // round-down add of MAGIC, leaving the code in the low mantissa bits.  t is monotonic in x,
+  // so when the group's extremes give t in [-1/2, L + 1/2) the clip is a no-op for every
+  // element (the usual case: zero and scale round the true min / range by < 2^-11).
+  const bool noclip = quot(mn) >= -0.5f && quot(mx) < (float)LEVELS + 0.5f;
+  if (noclip) {
 #pragma unroll
-  for (int k = 0; k < BITS; ++k) {
-    uint32_t word = 0u;
+    for (int k = 0; k < BITS; ++k) {
+      uint32_t word = 0u;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const float d = __fsub_rn(x[PER * k + i], zero);
-      const float q = __fmul_rn(d, y);
-      const float t = __fmaf_rn(__fmaf_rn(-q, scale, d), y, q);
-      // clip(round_half_away(t), 0, L) == floor(fl(clip(t, 0, L) + 1/2)); the floor comes
-      // from a round-down add of MAGIC, leaving the code in the low mantissa bits
-      const float a = __fadd_rn(fminf(fmaxf(t, 0.f), (float)LEVELS), 0.5f);
-      word |= (__float_as_uint(__fadd_rd(a, MAGIC)) & (uint32_t)LEVELS) << (BITS * i);
+      for (int i = 0; i < PER; ++i) {
+        const float a = __fadd_rn(quot(x[PER * k + i]), 0.5f);
+        word |= (__float_as_uint(__fadd_rd(a, MAGIC)) & (uint32_t)LEVELS) << (BITS * i);
+      }
+      w[k] = word;
     }
-    w[k] = word;
+  } else {
+#pragma unroll
+    for (int k = 0; k < BITS; ++k) {
+      uint32_t word = 0u;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const float a = __fadd_rn(fminf(fmaxf(quot(x[PER * k + i]), 0.f), (float)LEVELS), 0.5f);
+        word |= (__float_as_uint(__fadd_rd(a, MAGIC)) & (uint32_t)LEVELS) << (BITS * i);
+      }
+      w[k] = word;
+    }
   }
   if (exact) {  // rare (inf / nan parameters): the reference arithmetic verbatim; cold, unrolled
 #pragma unroll
