@@ -1,0 +1,181 @@
+"""Split-K mixed INT2/INT4 flash-decode attention over the device pool.
+
+Drop-in for the decode half of /root/reference/pkg/src/kvmix/attention.py:
+``flash_decode`` keeps its signature (:175) and validation order (:188-201) and
+returns a numpy [H, d] float32 array like the reference; ``merge_partials`` (:154)
+and ``SplitPartial`` (:145) keep their meaning.  The work is done by the sm_100a
+kernel K2 of libkvmix_b200 (tensor-core split decode; CTAs stream byte-balanced tile
+ranges and the last CTA of a split (request, kv head) merges its partials -- the
+combine K3 is fused in).
+
+``DecodeBatch`` / ``flash_decode_batched`` are the native hot-path API: a batch of
+requests, one layer per call, q/out as device tensors, page tables resident on the
+device, no host synchronisation.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import lib
+from .errors import ValidationError
+from .plan import NUM_SMS_B200, plan_stream
+from .pool import MixedPrecisionPool, PageTable, csr_tables, split_partitioned
+
+VARIANT_TENSOR_CORE = 0
+VARIANT_SIMPLE = 1
+
+
+@dataclass
+class SplitPartial:
+    """Per-split attention state for one query head (attention.py:145-151)."""
+
+    acc: np.ndarray
+    lse: float
+    max_logit: float
+
+
+def merge_partials(parts: Sequence[SplitPartial]) -> np.ndarray:
+    """attention.py:154-165, on the GPU (natural-log domain, fp32)."""
+    if not parts:
+        raise ValidationError("cannot merge an empty partial list")
+    dev = _lib.require_cuda()
+    acc = torch.as_tensor(np.stack([np.asarray(p.acc, dtype=np.float32) for p in parts]), device=dev)
+    lse = torch.tensor([p.lse for p in parts], dtype=torch.float32, device=dev)
+    mx = torch.tensor([p.max_logit for p in parts], dtype=torch.float32, device=dev)
+    out = torch.empty(acc.shape[1], dtype=torch.float32, device=dev)
+    _lib.check(lib.kvmix_merge_partials(acc.data_ptr(), lse.data_ptr(), mx.data_ptr(), acc.shape[0],
+                                        acc.shape[1], out.data_ptr(), _lib.stream()))
+    return out.cpu().numpy()
+
+
+class DecodeBatch:
+    """Device-resident CSR page tables + stream-K plan (pieces, CTA ranges, partial slots,
+    arrival counters) for a request batch.  One batch is used on one stream at a time."""
+
+    def __init__(self, pool: MixedPrecisionPool, request_ids=None, n_q_heads: int | None = None,
+                 tables: list | None = None, **plan_kw):
+        self.pool = pool
+        cfg = pool.config
+        self.n_q_heads = n_q_heads or cfg.n_kv_heads
+        if self.n_q_heads % cfg.n_kv_heads:
+            raise ValidationError("n_heads not a multiple of the pool's n_kv_heads")
+        if self.n_q_heads // cfg.n_kv_heads > 8:
+            raise ValidationError("GQA group larger than 8 is not supported on device")
+        self.request_ids = list(request_ids) if request_ids is not None else None
+        self._tables = tables
+        self.plan_kw = plan_kw
+        self.refresh()
+
+    def refresh(self) -> None:
+        """Rebuild device tables and the plan (after appends / new requests)."""
+        pool, cfg = self.pool, self.pool.config
+        if self._tables is not None:
+            parts = [split_partitioned(t.slots if isinstance(t, PageTable) else np.asarray(t), cfg.offset,
+                                       cfg.page_size) for t in self._tables]
+            t = csr_tables([p for p, _ in parts], [i for _, i in parts], pool.device)
+        else:
+            t = pool.device_tables(self.request_ids)
+        self.batch = int(t["n_pages"].size)
+        self.csr = t
+        kw = dict(self.plan_kw)
+        if "n_cta" not in kw:
+            n_sm = NUM_SMS_B200
+            if pool.device is not None and pool.device.type == "cuda":
+                n_sm = torch.cuda.get_device_properties(pool.device).multi_processor_count
+            kw["n_cta"] = n_sm * int(kw.pop("ctas_per_sm", 3))
+        else:
+            kw.pop("ctas_per_sm", None)
+        work, cta_ptr, n_parts = plan_stream(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride,
+                                             pool.slot_stride, **kw)
+        dev = pool.device
+        self.work = torch.as_tensor(work, device=dev)
+        self.cta_ptr = torch.as_tensor(cta_ptr, device=dev)
+        self.n_cta = int(cta_ptr.size - 1)
+        self.n_pieces = int(work.shape[0])
+        self.n_parts = n_parts
+        self.partials = torch.empty(max(1, n_parts) * 8 * (cfg.head_dim + 2), dtype=torch.float32, device=dev)
+        self.counters = torch.zeros(self.batch * cfg.n_kv_heads, dtype=torch.int32, device=dev)
+        self.n_tokens = t["n_pages"] * cfg.page_size + t["n_int4"]
+
+    def kv_bytes(self) -> int:
+        """Algorithmic KV bytes one layer's decode reads (all kv heads)."""
+        cfg = self.pool.config
+        from .quant import key_page_payload_bytes, token_block_payload_bytes
+        per_page = key_page_payload_bytes(cfg.head_dim) + 32 * token_block_payload_bytes(cfg.head_dim, 2)
+        per_int4 = 2 * token_block_payload_bytes(cfg.head_dim, 4)
+        return int(cfg.n_kv_heads * (self.csr["n_pages"].sum() * per_page + self.csr["n_int4"].sum() * per_int4))
+
+
+def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: torch.Tensor | None = None,
+                         scale: float | None = None, variant: int = VARIANT_TENSOR_CORE) -> torch.Tensor:
+    """Decode attention for every request of ``batch`` at ``layer``.
+
+    q: [B, n_q_heads, d] device tensor (f32/bf16/f16); returns out [B, n_q_heads, d]
+    (dtype of q unless ``out`` is given).  Asynchronous on the current stream.
+    """
+    pool, cfg = batch.pool, batch.pool.config
+    if q.dim() != 3 or q.shape[0] != batch.batch or q.shape[1] != batch.n_q_heads or q.shape[2] != cfg.head_dim:
+        raise ValidationError(f"q must be [{batch.batch}, {batch.n_q_heads}, {cfg.head_dim}]")
+    if not 0 <= layer < cfg.n_layers:
+        raise ValidationError("layer out of range")
+    if not q.is_contiguous():
+        q = q.contiguous()
+    if out is None:
+        out = torch.empty_like(q)
+    if scale is None:
+        scale = 1.0 / math.sqrt(cfg.head_dim)
+    t = batch.csr
+    _lib.check(lib.kvmix_flash_decode(
+        q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
+        pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,
+        batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
+        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
+        batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), int(variant),
+        _lib.stream()))
+    return out
+
+
+def flash_decode(q, page_table, pool_view, split_len: int = 128, scale=None, variant: int = VARIANT_TENSOR_CORE):
+    """attention.py:175-218 drop-in: single-query decode over a partitioned page table.
+
+    ``split_len`` is validated like the reference but the device kernel chooses its own
+    bitwidth-homogeneous split (a page or 32 INT4 slots per tile); results are
+    split-invariant up to float rounding, as the reference's are.
+    """
+    is_torch = isinstance(q, torch.Tensor)
+    qn = q if is_torch else np.asarray(q, dtype=np.float32)
+    if qn.ndim != 2:
+        raise ValidationError("q must be [n_heads, d]")
+    n_heads, d = qn.shape
+    slots = page_table.slots if isinstance(page_table, PageTable) else \
+        np.asarray([a.index for a in page_table.entries], dtype=np.int64)
+    if slots.size == 0:
+        raise ValidationError("empty page table")
+    if split_len < 1:
+        raise ValidationError("split_len must be >= 1")
+    pool = pool_view.pool
+    cfg = pool.config
+    is2 = slots < cfg.offset
+    if np.any(is2[int(is2.sum()):]):
+        raise ValidationError("page table not partitioned: INT4 address precedes INT2")
+    n_kv = cfg.n_kv_heads
+    if n_heads % n_kv != 0:
+        raise ValidationError("n_heads not a multiple of the pool's n_kv_heads")
+    if d != cfg.head_dim:
+        raise ValidationError("q head dim does not match the pool")
+    in_range = (slots >= 0) & (slots < cfg.total_slots)
+    if not np.all(in_range) or np.any(pool._owner[slots] < 0):
+        raise ValidationError("dangling slot address")
+    pool._require_written(slots, pool_view.layer)
+    batch = DecodeBatch(pool, n_q_heads=n_heads, tables=[slots])
+    qd = (q if is_torch else torch.as_tensor(qn)).to(pool.device, torch.float32).reshape(1, n_heads, d)
+    out = flash_decode_batched(qd, batch, pool_view.layer, scale=scale, variant=variant)
+    res = out[0]
+    return res if is_torch else res.cpu().numpy()

@@ -1,0 +1,574 @@
+// K1 (quantize + pack), K4 data half (INT4 append), K5 (gather-dequant) and the
+// generic codec entry points.  Bit-exact with /root/reference/pkg/src/kvmix/quant.py:
+// every op in the group arithmetic is an explicit round-to-nearest intrinsic
+// (__fsub_rn / __fdiv_rn / __fadd_rn / __float2half_rn), so no contraction or
+// fast-math can change a code, scale or zero.
+#include "common.cuh"
+#include "launch.h"
+
+namespace kvmix {
+
+// ---------------------------------------------------------------------------------
+// One warp encodes one token vector x[0..D) as a TokenBlock (quant.py:189-232):
+// lane owns channels [lane*CPL, lane*CPL+CPL); groups of 32 channels are reduced
+// with segmented shuffles; codes are OR-reduced into 32-bit words.  `st` places the
+// payload: st.code(word_index, word) gets code bytes [4w, 4w+4), st.param(j, s, z)
+// the fp16 bits of group j's (scale, zero).
+template <int D, int BITS, typename Store>
+__device__ __forceinline__ void encode_token_warp(const float (&v)[D / 32], const Store& st, int lane, int32_t* err) {
+  constexpr int CPL = D / 32;               // channels per lane
+  constexpr int LPG = 32 / CPL;             // lanes per group of 32 channels
+  constexpr int LPW = 32 / (BITS * CPL);    // lanes per 32-bit code word
+  constexpr int LEVELS = (1 << BITS) - 1;
+  float mn = v[0], mx = v[0];
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    mn = fminf(mn, v[i]);
+    mx = fmaxf(mx, v[i]);
+    finite &= isfinite(v[i]);
+  }
+#pragma unroll
+  for (int o = 1; o < LPG; o <<= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (!finite && err) atomicOr(err, 1);
+  float scale, zero;
+  group_params(mn, mx, LEVELS, scale, zero);
+  uint32_t bits = 0;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) bits |= quant_code(v[i], scale, zero, LEVELS) << (BITS * i);
+  uint32_t word = bits << (BITS * CPL * (lane % LPW));
+#pragma unroll
+  for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+  if (lane % LPW == 0) st.code(lane / LPW, word);
+  if (lane % LPG == 0) st.param(lane / LPG, pack_param(scale, zero));
+}
+
+// Thread c of a block encodes channel c of one KeyPageBlock (quant.py:160-177): 32
+// token values of one channel -> code bytes tau = 0..7 (tokens 4tau..4tau+3) stored in
+// KC row tau, (scale, zero) into KS / KZ (device record layout, common.cuh).
+template <int D>
+__device__ __forceinline__ void encode_key_channel(const float (&x)[G], uint8_t* rec, int c, int32_t* err) {
+  float mn = x[0], mx = x[0];
+  bool finite = true;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    mn = fminf(mn, x[j]);
+    mx = fmaxf(mx, x[j]);
+    finite &= isfinite(x[j]);
+  }
+  if (!finite && err) atomicOr(err, 1);
+  float scale, zero;
+  group_params(mn, mx, 3, scale, zero);
+  uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    w0 |= quant_code(x[j], scale, zero, 3) << (2 * j);
+    w1 |= quant_code(x[j + 16], scale, zero, 3) << (2 * j);
+  }
+#pragma unroll
+  for (int tau = 0; tau < 8; ++tau) rec[pg_kc_off(D, tau, c)] = (uint8_t)(((tau < 4 ? w0 : w1) >> (8 * (tau & 3))) & 0xffu);
+  const uint32_t pz = pack_param(scale, zero);
+  reinterpret_cast<uint16_t*>(rec + PG_KS(D))[pg_kp_idx(D, c)] = (uint16_t)(pz & 0xffffu);
+  reinterpret_cast<uint16_t*>(rec + PG_KZ(D))[pg_kp_idx(D, c)] = (uint16_t)(pz >> 16);
+}
+
+// TokenBlock placement inside a staged INT2 page record (token row t of the page).
+template <int D>
+struct PageVStore {
+  uint8_t* rec;
+  int t;
+  __device__ void code(int w, uint32_t word) const {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rec[PG_VC(D) + pg_vc_off(D, t, 4 * w + k)] = (uint8_t)(word >> (8 * k));
+  }
+  __device__ void param(int j, uint32_t pz) const {
+    reinterpret_cast<uint16_t*>(rec + PG_VS(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + PG_VZ(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz >> 16);
+  }
+};
+// INT4 TokenBlock placement inside a staged slot record: K (V = false) or V half.
+template <int D, bool V>
+struct SlotStore {
+  uint8_t* rec;
+  __device__ void code(int w, uint32_t word) const {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = 4 * w + k;
+      rec[V ? SL_VC(D) + sl_vc_off(D, i) : sl_kc_off(D, i)] = (uint8_t)(word >> (8 * k));
+    }
+  }
+  __device__ void param(int j, uint32_t pz) const {
+    reinterpret_cast<uint16_t*>(rec + (V ? SL_VS(D) : SL_KS(D)))[j] = (uint16_t)(pz & 0xffffu);
+    reinterpret_cast<uint16_t*>(rec + (V ? SL_VZ(D) : SL_KZ(D)))[j] = (uint16_t)(pz >> 16);
+  }
+};
+
+// ------------------------------ generic codec ----------------------------------------
+// Runtime head_dim (any d for key pages -- LAYOUT.md's worked example has d = 2 --,
+// any multiple of 32 for token blocks).  These back the single-block reference API.
+__global__ void encode_key_pages_kernel(const float* __restrict__ keys, int64_t n_pages, int d,
+                                        uint8_t* __restrict__ out, int64_t out_stride, int32_t* err) {
+  const int64_t p = blockIdx.x;
+  uint8_t* blk = out + p * out_stride;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float x[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) x[j] = keys[(p * G + j) * d + c];
+    float mn = x[0], mx = x[0];
+    bool finite = true;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      mn = fminf(mn, x[j]);
+      mx = fmaxf(mx, x[j]);
+      finite &= isfinite(x[j]);
+    }
+    if (!finite && err) atomicOr(err, 1);
+    float scale, zero;
+    group_params(mn, mx, 3, scale, zero);
+    uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      w0 |= quant_code(x[j], scale, zero, 3) << (2 * j);
+      w1 |= quant_code(x[j + 16], scale, zero, 3) << (2 * j);
+    }
+    reinterpret_cast<uint32_t*>(blk)[2 * c] = w0;
+    reinterpret_cast<uint32_t*>(blk)[2 * c + 1] = w1;
+    reinterpret_cast<uint32_t*>(blk + 8 * (int64_t)d)[c] = pack_param(scale, zero);
+  }
+}
+
+// warp per token; group j of 32 channels handled with lane = channel
+__global__ void encode_token_blocks_kernel(const float* __restrict__ x, int64_t n, int d, int bits,
+                                           uint8_t* __restrict__ out, int64_t out_stride, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (t >= n) return;
+  const int levels = (1 << bits) - 1;
+  const int lpw = 32 / bits;  // lanes per 32-bit code word
+  uint8_t* blk = out + t * out_stride;
+  for (int j = 0; j < d / G; ++j) {
+    const float v = x[t * d + j * G + lane];
+    float mn = v, mx = v;
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (!isfinite(v) && err) atomicOr(err, 1);
+    float scale, zero;
+    group_params(mn, mx, levels, scale, zero);
+    uint32_t word = quant_code(v, scale, zero, levels) << (bits * (lane % lpw));
+    for (int o = 1; o < lpw; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+    if (lane % lpw == 0) reinterpret_cast<uint32_t*>(blk)[j * bits + lane / lpw] = word;
+    if (lane == 0) reinterpret_cast<uint32_t*>(blk + d * bits / 8)[j] = pack_param(scale, zero);
+  }
+}
+
+__global__ void decode_key_pages_kernel(const uint8_t* __restrict__ blocks, int64_t n_pages, int d,
+                                        int64_t in_stride, float* __restrict__ out) {
+  const int64_t p = blockIdx.x;
+  const uint8_t* b = blocks + p * in_stride;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    const uint32_t w0 = reinterpret_cast<const uint32_t*>(b)[2 * c];
+    const uint32_t w1 = reinterpret_cast<const uint32_t*>(b)[2 * c + 1];
+    const uint32_t pr = reinterpret_cast<const uint32_t*>(b + 8 * (int64_t)d)[c];
+    const float s = __half2float(__ushort_as_half((unsigned short)(pr & 0xffff)));
+    const float z = __half2float(__ushort_as_half((unsigned short)(pr >> 16)));
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const uint32_t code = ((j < 16 ? w0 : w1) >> (2 * (j & 15))) & 3u;
+      out[(p * G + j) * d + c] = __fmaf_rn((float)code, s, z);  // code*scale exact, one rounding
+    }
+  }
+}
+
+// thread per (block, channel)
+__global__ void decode_token_blocks_kernel(const uint8_t* __restrict__ blocks, int64_t n, int d, int bits,
+                                           int64_t in_stride, float* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * d) return;
+  int64_t t = i / d;
+  int c = (int)(i % d);
+  const uint8_t* b = blocks + t * in_stride;
+  uint32_t byte = b[c * bits / 8];
+  uint32_t code = (byte >> ((c * bits) & 7)) & ((1u << bits) - 1);
+  const uint8_t* pp = b + d * bits / 8 + 4 * (c / G);
+  uint32_t pr = (uint32_t)pp[0] | ((uint32_t)pp[1] << 8) | ((uint32_t)pp[2] << 16) | ((uint32_t)pp[3] << 24);
+  float s = __half2float(__ushort_as_half((unsigned short)(pr & 0xffff)));
+  float z = __half2float(__ushort_as_half((unsigned short)(pr >> 16)));
+  out[i] = __fmaf_rn((float)code, s, z);
+}
+
+// One warp per ragged group (quant.py:64-87).
+__global__ void quantize_groups_kernel(const float* __restrict__ x, const int64_t* __restrict__ offsets,
+                                       int64_t n_groups, int bits, uint8_t* __restrict__ codes,
+                                       float* __restrict__ scale_out, float* __restrict__ zero_out, int32_t* err) {
+  int lane = threadIdx.x & 31;
+  int64_t gi = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gi >= n_groups) return;
+  int64_t lo = offsets[gi], hi = offsets[gi + 1];
+  float mn = INFINITY, mx = -INFINITY;
+  bool finite = true;
+  for (int64_t i = lo + lane; i < hi; i += 32) {
+    float v = x[i];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+    finite &= isfinite(v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (!finite && err) atomicOr(err, 1);
+  int levels = (1 << bits) - 1;
+  float s, z;
+  group_params(mn, mx, levels, s, z);
+  for (int64_t i = lo + lane; i < hi; i += 32) codes[i] = (uint8_t)quant_code(x[i], s, z, levels);
+  if (lane == 0) {
+    scale_out[gi] = s;
+    zero_out[gi] = z;
+  }
+}
+
+// thread per output byte (quant.py:96-109)
+__global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t n, int bits, uint8_t* __restrict__ out,
+                                  int32_t* err) {
+  int per = 8 / bits;
+  int64_t nb = (n + per - 1) / per;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  uint32_t byte = 0;
+  for (int k = 0; k < per; ++k) {
+    int64_t j = i * per + k;
+    if (j < n) {
+      uint32_t c = codes[j];
+      if (c >= (1u << bits) && err) atomicOr(err, 2);
+      byte |= (c & ((1u << bits) - 1)) << (bits * k);
+    }
+  }
+  out[i] = (uint8_t)byte;
+}
+
+__global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t n, int bits, uint8_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int per = 8 / bits;
+  out[i] = (packed[i / per] >> (bits * (i % per))) & ((1u << bits) - 1);
+}
+
+// ------------------------------ pool data plane ----------------------------------------
+// write_prefill INT2 branch (pool.py:236-252 -> write_page :201-215): one block per
+// (request page, kv head, layer).  Threads c < D encode the KeyPageBlock column c;
+// the 4 warps encode the page's 32 INT2 V TokenBlocks.  The record is assembled in
+// shared memory in the device layout and leaves with coalesced 16-byte stores.
+template <int D, typename T>
+__global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
+                                                            int64_t n_tokens, int64_t n_kv_heads,
+                                                            const int32_t* __restrict__ page_tokens,
+                                                            const int32_t* __restrict__ page_ids,
+                                                            uint8_t* __restrict__ int2_pool, int64_t pool_pages,
+                                                            int32_t* err) {
+  const int p = blockIdx.x, h = blockIdx.y, l = blockIdx.z;
+  __shared__ int tok[G];
+  __shared__ __align__(16) uint8_t srec[page_stride(D)];
+  if (threadIdx.x < G) tok[threadIdx.x] = page_tokens[(int64_t)p * G + threadIdx.x];
+  __syncthreads();
+  const int64_t page = page_ids[p];
+  uint8_t* rec = int2_pool + (((int64_t)l * n_kv_heads + h) * pool_pages + page) * page_stride(D);
+  auto elem = [&](int t, int c) -> int64_t { return (((int64_t)l * n_tokens + t) * n_kv_heads + h) * D + c; };
+  for (int c = threadIdx.x; c < D; c += 128) {
+    float x[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) x[j] = to_f32(keys[elem(tok[j], c)]);
+    encode_key_channel<D>(x, srec, c, err);
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+  for (int j = warp; j < G; j += 4) {
+    float v[D / 32];
+#pragma unroll
+    for (int i = 0; i < D / 32; ++i) v[i] = to_f32(values[elem(tok[j], lane * (D / 32) + i)]);
+    encode_token_warp<D, 2>(v, PageVStore<D>{srec, j}, lane, err);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < page_stride(D) / 16; i += 128)
+    reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
+}
+
+// INT4 tokens: write_prefill :253-262, write_token :217-226, append_decode_token :284-306.
+// Warp per (token, kv head, layer); input element (l, t, h, c) at
+// ((t_stride_l * l) + t * tok_stride + h * D + c) with explicit strides.  The slot
+// record is staged per warp in shared memory (device layout) and stored as 16 B words.
+template <int D, typename T>
+__global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ keys, const T* __restrict__ values,
+                                                          int64_t n, int64_t layer_stride, int64_t tok_stride,
+                                                          int64_t n_kv_heads, int64_t layer0,
+                                                          const int32_t* __restrict__ tokens,
+                                                          const int32_t* __restrict__ int4_ids,
+                                                          uint8_t* __restrict__ int4_pool, int64_t pool_int4,
+                                                          int32_t* err) {
+  constexpr int SS = slot_stride(D);
+  __shared__ __align__(16) uint8_t srec[4][SS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x / 32;
+  const int64_t i = (int64_t)blockIdx.x * 4 + warp;
+  const int h = blockIdx.y, l = blockIdx.z;
+  if (i >= n) return;
+  uint8_t* st = srec[warp];
+  for (int k = lane; k < SS / 4; k += 32) reinterpret_cast<uint32_t*>(st)[k] = 0u;  // padding stays zero
+  __syncwarp();
+  const int64_t t = tokens ? tokens[i] : i;
+  const int64_t base = l * layer_stride + t * tok_stride + (int64_t)h * D + lane * (D / 32);
+  uint8_t* rec =
+      int4_pool + (((layer0 + l) * n_kv_heads + h) * pool_int4 + (int64_t)int4_ids[i]) * SS;
+  float v[D / 32];
+#pragma unroll
+  for (int k = 0; k < D / 32; ++k) v[k] = to_f32(keys[base + k]);
+  encode_token_warp<D, 4>(v, SlotStore<D, false>{st}, lane, err);
+#pragma unroll
+  for (int k = 0; k < D / 32; ++k) v[k] = to_f32(values[base + k]);
+  encode_token_warp<D, 4>(v, SlotStore<D, true>{st}, lane, err);
+  __syncwarp();
+  if (lane < SS / 16) reinterpret_cast<uint4*>(rec)[lane] = reinterpret_cast<const uint4*>(st)[lane];
+}
+
+// K5 gather-dequant (pool.py:394-439): thread per (slot, head, channel) -> f32 k/v.
+template <int D>
+__global__ void gather_dequant_kernel(const uint8_t* __restrict__ int2_pool, const uint8_t* __restrict__ int4_pool,
+                                      int64_t pool_pages, int64_t pool_int4, int64_t offset, int64_t layer,
+                                      int64_t n_kv_heads, const int32_t* __restrict__ slots, int64_t m,
+                                      float* __restrict__ k_out, float* __restrict__ v_out) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * n_kv_heads * D) return;
+  const int c = (int)(idx % D);
+  const int64_t h = (idx / D) % n_kv_heads;
+  const int64_t i = idx / (D * n_kv_heads);
+  const int64_t slot = slots[i];
+  auto half_at = [](const uint8_t* p, int idx) {
+    return __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(p)[idx]));
+  };
+  float kv, vv;
+  if (slot < offset) {
+    const int64_t page = slot / G;
+    const int row = (int)(slot % G);
+    const uint8_t* rec = int2_pool + ((layer * n_kv_heads + h) * pool_pages + page) * page_stride(D);
+    const uint32_t kc = (rec[pg_kc_off(D, row >> 2, c)] >> (2 * (row & 3))) & 3u;
+    kv = __fmaf_rn((float)kc, half_at(rec + PG_KS(D), pg_kp_idx(D, c)), half_at(rec + PG_KZ(D), pg_kp_idx(D, c)));
+    const uint32_t vc = (rec[PG_VC(D) + pg_vc_off(D, row, c >> 2)] >> (2 * (c & 3))) & 3u;
+    const int pj = pg_vp_idx(D, row, c / G);
+    vv = __fmaf_rn((float)vc, half_at(rec + PG_VS(D), pj), half_at(rec + PG_VZ(D), pj));
+  } else {
+    const uint8_t* rec = int4_pool + ((layer * n_kv_heads + h) * pool_int4 + (slot - offset)) * slot_stride(D);
+    const int sh = 4 * (c & 1);
+    const uint32_t kc = (rec[sl_kc_off(D, c >> 1)] >> sh) & 15u;
+    kv = __fmaf_rn((float)kc, half_at(rec + SL_KS(D), c / G), half_at(rec + SL_KZ(D), c / G));
+    const uint32_t vc = (rec[SL_VC(D) + sl_vc_off(D, c >> 1)] >> sh) & 15u;
+    vv = __fmaf_rn((float)vc, half_at(rec + SL_VS(D), c / G), half_at(rec + SL_VZ(D), c / G));
+  }
+  k_out[idx] = kv;
+  v_out[idx] = vv;
+}
+
+}  // namespace kvmix
+
+// =============================== C ABI ===============================================
+using namespace kvmix;
+
+#define DISPATCH_D(d, ...)                                   \
+  switch (d) {                                               \
+    case 32: { constexpr int D = 32; __VA_ARGS__; } break;   \
+    case 64: { constexpr int D = 64; __VA_ARGS__; } break;   \
+    case 128: { constexpr int D = 128; __VA_ARGS__; } break; \
+    case 256: { constexpr int D = 256; __VA_ARGS__; } break; \
+    default: return fail(KVMIX_EINVAL, "head_dim must be 32, 64, 128 or 256");  \
+  }
+
+extern "C" int64_t kvmix_page_stride(int64_t d) { return page_stride((int)d); }
+extern "C" int64_t kvmix_slot_stride(int64_t d) { return slot_stride((int)d); }
+// Host-side export of the record permutation the kernels use (same constexpr helpers).
+extern "C" int kvmix_page_layout(int64_t d, int64_t* perm) {
+  if (d < 32 || d > 256 || d % 32) return fail(KVMIX_EINVAL, "head_dim must be 32, 64, 128 or 256");
+  const int D = (int)d, ng = D / 32, kp = key_page_bytes(D), tb2 = tok_bytes(D, 2);
+  for (int i = 0; i < page_stride(D); ++i) perm[i] = -1;
+  for (int c = 0; c < D; ++c) {
+    for (int tau = 0; tau < 8; ++tau) perm[pg_kc_off(D, tau, c)] = 8 * c + tau;
+    for (int k = 0; k < 2; ++k) {
+      perm[PG_KS(D) + 2 * pg_kp_idx(D, c) + k] = 8 * D + 4 * c + k;
+      perm[PG_KZ(D) + 2 * pg_kp_idx(D, c) + k] = 8 * D + 4 * c + 2 + k;
+    }
+  }
+  for (int t = 0; t < G; ++t) {
+    for (int b = 0; b < D / 4; ++b) perm[PG_VC(D) + pg_vc_off(D, t, b)] = kp + t * tb2 + b;
+    for (int j = 0; j < ng; ++j)
+      for (int k = 0; k < 2; ++k) {
+        perm[PG_VS(D) + 2 * pg_vp_idx(D, t, j) + k] = kp + t * tb2 + D / 4 + 4 * j + k;
+        perm[PG_VZ(D) + 2 * pg_vp_idx(D, t, j) + k] = kp + t * tb2 + D / 4 + 4 * j + 2 + k;
+      }
+  }
+  return KVMIX_OK;
+}
+
+extern "C" int kvmix_slot_layout(int64_t d, int64_t* perm) {
+  if (d < 32 || d > 256 || d % 32) return fail(KVMIX_EINVAL, "head_dim must be 32, 64, 128 or 256");
+  const int D = (int)d, ng = D / 32, tb4 = tok_bytes(D, 4);
+  for (int i = 0; i < slot_stride(D); ++i) perm[i] = -1;
+  for (int i = 0; i < D / 2; ++i) {
+    perm[sl_kc_off(D, i)] = i;
+    perm[SL_VC(D) + sl_vc_off(D, i)] = tb4 + i;
+  }
+  for (int j = 0; j < ng; ++j)
+    for (int k = 0; k < 2; ++k) {
+      perm[SL_KS(D) + 2 * j + k] = D / 2 + 4 * j + k;
+      perm[SL_KZ(D) + 2 * j + k] = D / 2 + 4 * j + 2 + k;
+      perm[SL_VS(D) + 2 * j + k] = tb4 + D / 2 + 4 * j + k;
+      perm[SL_VZ(D) + 2 * j + k] = tb4 + D / 2 + 4 * j + 2 + k;
+    }
+  return KVMIX_OK;
+}
+
+extern "C" int64_t kvmix_key_page_payload_bytes(int64_t d) { return key_page_bytes((int)d); }
+extern "C" int64_t kvmix_token_block_payload_bytes(int64_t d, int64_t b) { return tok_bytes((int)d, (int)b); }
+
+extern "C" int kvmix_encode_key_pages(const float* keys, int64_t n_pages, int64_t d, uint8_t* out,
+                                      int64_t out_stride, int32_t* err, void* stream) {
+  if (n_pages == 0) return KVMIX_OK;
+  if (d <= 0 || out_stride % 4 || out_stride < key_page_bytes((int)d)) return fail(KVMIX_EINVAL, "bad key page shape");
+  encode_key_pages_kernel<<<(unsigned)n_pages, 128, 0, (cudaStream_t)stream>>>(keys, n_pages, (int)d, out,
+                                                                               out_stride, err);
+  return check_launch("encode_key_pages");
+}
+
+extern "C" int kvmix_encode_token_blocks(const float* x, int64_t n, int64_t d, int32_t bits, uint8_t* out,
+                                         int64_t out_stride, int32_t* err, void* stream) {
+  if (n == 0) return KVMIX_OK;
+  if (bits != 2 && bits != 4) return fail(KVMIX_EINVAL, "unsupported bitwidth");
+  if (d <= 0 || d % G) return fail(KVMIX_EINVAL, "head dim not divisible by the group size");
+  if (out_stride % 4) return fail(KVMIX_EINVAL, "out_stride must be a multiple of 4");
+  encode_token_blocks_kernel<<<(unsigned)((n + 3) / 4), 128, 0, (cudaStream_t)stream>>>(x, n, (int)d, bits, out,
+                                                                                        out_stride, err);
+  return check_launch("encode_token_blocks");
+}
+
+extern "C" int kvmix_decode_key_pages(const uint8_t* blocks, int64_t n_pages, int64_t d, int64_t in_stride,
+                                      float* out, void* stream) {
+  if (n_pages == 0) return KVMIX_OK;
+  if (d <= 0 || in_stride % 4) return fail(KVMIX_EINVAL, "bad key page shape");
+  decode_key_pages_kernel<<<(unsigned)n_pages, 128, 0, (cudaStream_t)stream>>>(blocks, n_pages, (int)d, in_stride,
+                                                                               out);
+  return check_launch("decode_key_pages");
+}
+
+extern "C" int kvmix_decode_token_blocks(const uint8_t* blocks, int64_t n, int64_t d, int32_t bits,
+                                         int64_t in_stride, float* out, void* stream) {
+  if (n == 0) return KVMIX_OK;
+  if (bits != 2 && bits != 4) return fail(KVMIX_EINVAL, "unsupported bitwidth");
+  if (d % G) return fail(KVMIX_EINVAL, "head_dim must be a multiple of 32");
+  int64_t total = n * d;
+  decode_token_blocks_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(blocks, n, (int)d,
+                                                                                                 bits, in_stride, out);
+  return check_launch("decode_token_blocks");
+}
+
+extern "C" int kvmix_quantize_groups(const float* x, const int64_t* offsets, int64_t n_groups, int32_t bits,
+                                     uint8_t* codes, float* scale, float* zero, int32_t* err, void* stream) {
+  if (n_groups == 0) return KVMIX_OK;
+  if (bits != 2 && bits != 4) return fail(KVMIX_EINVAL, "unsupported bitwidth");
+  quantize_groups_kernel<<<(unsigned)((n_groups + 3) / 4), 128, 0, (cudaStream_t)stream>>>(x, offsets, n_groups,
+                                                                                            bits, codes, scale, zero,
+                                                                                            err);
+  return check_launch("quantize_groups");
+}
+
+extern "C" int kvmix_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out, int32_t* err,
+                                void* stream) {
+  if (n == 0) return KVMIX_OK;
+  if (bits != 2 && bits != 4) return fail(KVMIX_EINVAL, "unsupported bitwidth");
+  int64_t nb = (n * bits + 7) / 8;
+  pack_codes_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, (cudaStream_t)stream>>>(codes, n, bits, out, err);
+  return check_launch("pack_codes");
+}
+
+extern "C" int kvmix_unpack_codes(const uint8_t* packed, int64_t n, int32_t bits, uint8_t* out, void* stream) {
+  if (n == 0) return KVMIX_OK;
+  if (bits != 2 && bits != 4) return fail(KVMIX_EINVAL, "unsupported bitwidth");
+  unpack_codes_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(packed, n, bits, out);
+  return check_launch("unpack_codes");
+}
+
+template <typename T>
+static int launch_prefill(const void* keys, const void* values, int64_t L, int64_t N, int64_t H, int64_t d,
+                          const int32_t* page_tokens, const int32_t* page_ids, int64_t np, const int32_t* int4_tokens,
+                          const int32_t* int4_ids, int64_t n4, uint8_t* int2_pool, int64_t pool_pages,
+                          uint8_t* int4_pool, int64_t pool_int4, int32_t* err, cudaStream_t s) {
+  const T* k = (const T*)keys;
+  const T* v = (const T*)values;
+  if (np > 0) {
+    dim3 grid((unsigned)np, (unsigned)H, (unsigned)L);
+    DISPATCH_D(d, prefill_pages_kernel<D, T><<<grid, 128, 0, s>>>(k, v, N, H, page_tokens, page_ids, int2_pool,
+                                                                  pool_pages, err));
+  }
+  if (n4 > 0) {
+    dim3 grid((unsigned)((n4 + 3) / 4), (unsigned)H, (unsigned)L);
+    DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>(k, v, n4, N * H * D, H * D, H, 0, int4_tokens,
+                                                                int4_ids, int4_pool, pool_int4, err));
+  }
+  return check_launch("write_prefill");
+}
+
+extern "C" int kvmix_write_prefill(const void* keys, const void* values, int32_t dtype, int64_t L, int64_t N,
+                                   int64_t H, int64_t d, const int32_t* page_tokens, const int32_t* page_ids,
+                                   int64_t np, const int32_t* int4_tokens, const int32_t* int4_ids, int64_t n4,
+                                   uint8_t* int2_pool, int64_t pool_pages, uint8_t* int4_pool, int64_t pool_int4,
+                                   int32_t* err, void* stream) {
+  if (L <= 0 || H <= 0 || H > 65535 || L > 65535) return fail(KVMIX_EINVAL, "bad layer/head counts");
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case KVMIX_F32:
+      return launch_prefill<float>(keys, values, L, N, H, d, page_tokens, page_ids, np, int4_tokens, int4_ids, n4,
+                                   int2_pool, pool_pages, int4_pool, pool_int4, err, s);
+    case KVMIX_BF16:
+      return launch_prefill<__nv_bfloat16>(keys, values, L, N, H, d, page_tokens, page_ids, np, int4_tokens,
+                                           int4_ids, n4, int2_pool, pool_pages, int4_pool, pool_int4, err, s);
+    case KVMIX_F16:
+      return launch_prefill<__half>(keys, values, L, N, H, d, page_tokens, page_ids, np, int4_tokens, int4_ids, n4,
+                                    int2_pool, pool_pages, int4_pool, pool_int4, err, s);
+    default:
+      return fail(KVMIX_EINVAL, "unsupported dtype");
+  }
+}
+
+template <typename T>
+static int launch_append(const void* k, const void* v, int64_t n, int64_t Lin, int64_t layer0, int64_t H, int64_t d,
+                         const int32_t* int4_ids, uint8_t* int4_pool, int64_t pool_int4, int32_t* err,
+                         cudaStream_t s) {
+  dim3 grid((unsigned)((n + 3) / 4), (unsigned)H, (unsigned)Lin);
+  DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>((const T*)k, (const T*)v, n, H * D, Lin * H * D, H,
+                                                              layer0, nullptr, int4_ids, int4_pool, pool_int4, err));
+  return check_launch("append_int4");
+}
+
+extern "C" int kvmix_append_int4(const void* k, const void* v, int32_t dtype, int64_t n, int64_t Lin,
+                                 int64_t layer0, int64_t L, int64_t H, int64_t d, const int32_t* int4_ids,
+                                 uint8_t* int4_pool, int64_t pool_int4, int32_t* err, void* stream) {
+  if (n == 0) return KVMIX_OK;
+  if (layer0 < 0 || layer0 + Lin > L) return fail(KVMIX_EINVAL, "layer range outside the pool");
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case KVMIX_F32: return launch_append<float>(k, v, n, Lin, layer0, H, d, int4_ids, int4_pool, pool_int4, err, s);
+    case KVMIX_BF16:
+      return launch_append<__nv_bfloat16>(k, v, n, Lin, layer0, H, d, int4_ids, int4_pool, pool_int4, err, s);
+    case KVMIX_F16: return launch_append<__half>(k, v, n, Lin, layer0, H, d, int4_ids, int4_pool, pool_int4, err, s);
+    default: return fail(KVMIX_EINVAL, "unsupported dtype");
+  }
+}
+
+extern "C" int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
+                                    int64_t pool_int4, int64_t offset, int64_t layer, int64_t H, int64_t d,
+                                    const int32_t* slots, int64_t m, float* k_out, float* v_out, void* stream) {
+  if (m == 0) return KVMIX_OK;
+  int64_t total = m * H * d;
+  unsigned grid = (unsigned)((total + 255) / 256);
+  DISPATCH_D(d, gather_dequant_kernel<D><<<grid, 256, 0, (cudaStream_t)stream>>>(
+                    int2_pool, int4_pool, pool_pages, pool_int4, offset, layer, H, slots, m, k_out, v_out));
+  return check_launch("gather_dequant");
+}

@@ -35,16 +35,6 @@ namespace kvmix {
 #ifndef KVMIX_SPLIT
 #define KVMIX_SPLIT 0
 #endif
-#ifndef KVMIX_PAIRS
-#define KVMIX_PAIRS 0
-#endif
-#ifndef KVMIX_META2
-#define KVMIX_META2 1  // tile metadata two tiles ahead (0: one tile ahead)
-#endif
-#ifndef KVMIX_BATCHIDS
-#define KVMIX_BATCHIDS 0  // 1: INT2 page ids 32 tiles per coalesced load (measured neutral)
-#endif
-constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
 constexpr int NW = 4;                 // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr float LOG2E = 1.4426950408889634f;
@@ -211,14 +201,11 @@ __device__ __forceinline__ uint32_t ld_s32(const uint8_t* base, int off) {
 // when some logit exceeds it by > RESCALE_SLACK (log2 units), so p <= 2^RESCALE_SLACK
 // stays well inside fp16 and the common path needs no cross-lane reduction -- only a
 // per-lane max and one vote.  The first tile of a piece establishes the max exactly.
-// When the max moved, `resc` is set (warp-uniform) and the accumulators must be
-// multiplied by (al0, al1) (0 on the first tile).
-__device__ __forceinline__ void softmax_p(float (&sv)[8], Softmax& st, uint32_t (&bP)[2][2], float& al0,
-                                          float& al1, bool& resc) {
+template <int D>
+__device__ __forceinline__ void softmax_tile(float (&sv)[8], Softmax& st, Acc<D>& acc, uint32_t (&bP)[2][2]) {
   float tm0 = fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6]));
   float tm1 = fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7]));
-  resc = __any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK);
-  if (resc) {
+  if (__any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK)) {
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
       tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
@@ -226,8 +213,16 @@ __device__ __forceinline__ void softmax_p(float (&sv)[8], Softmax& st, uint32_t 
     }
     // first tile: shift to its max (acc is still zero); later: raise only, by max(tm, 0)
     const float sh0 = st.init ? fmaxf(tm0, 0.f) : tm0, sh1 = st.init ? fmaxf(tm1, 0.f) : tm1;
-    al0 = st.init ? fast_exp2(-sh0) : 0.f;
-    al1 = st.init ? fast_exp2(-sh1) : 0.f;
+    const float al0 = st.init ? fast_exp2(-sh0) : 0.f, al1 = st.init ? fast_exp2(-sh1) : 0.f;
+#pragma unroll
+    for (int m = 0; m < D / 16; ++m) {
+      acc.o[m][0] *= al0; acc.o[m][2] *= al0;
+      acc.o[m][1] *= al1; acc.o[m][3] *= al1;
+    }
+    acc.zs[0] *= al0; acc.zs[2] *= al0;
+    acc.zs[1] *= al1; acc.zs[3] *= al1;
+    acc.zs2[0] *= al0; acc.zs2[2] *= al0;
+    acc.zs2[1] *= al1; acc.zs2[3] *= al1;
     st.m0 += sh0;
     st.m1 += sh1;
     st.init = true;
@@ -245,69 +240,6 @@ __device__ __forceinline__ void softmax_p(float (&sv)[8], Softmax& st, uint32_t 
   bP[0][1] = movtrans(pack_h2(p[2], p[3]));
   bP[1][0] = movtrans(pack_h2(p[4], p[5]));
   bP[1][1] = movtrans(pack_h2(p[6], p[7]));
-}
-
-// Two tiles' logits at once (one vote, one optional rescale for 64 tokens).
-__device__ __forceinline__ void softmax_p2(float (&sv)[8], float (&sw)[8], Softmax& st, uint32_t (&bP)[2][2],
-                                           uint32_t (&bQ)[2][2], float& al0, float& al1, bool& resc) {
-  float tm0 = fmaxf(fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6])), fmaxf(fmaxf(sw[0], sw[2]), fmaxf(sw[4], sw[6])));
-  float tm1 = fmaxf(fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7])), fmaxf(fmaxf(sw[1], sw[3]), fmaxf(sw[5], sw[7])));
-  resc = __any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK);
-  if (resc) {
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
-      tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
-    }
-    const float sh0 = st.init ? fmaxf(tm0, 0.f) : tm0, sh1 = st.init ? fmaxf(tm1, 0.f) : tm1;
-    al0 = st.init ? fast_exp2(-sh0) : 0.f;
-    al1 = st.init ? fast_exp2(-sh1) : 0.f;
-    st.m0 += sh0;
-    st.m1 += sh1;
-    st.init = true;
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-      sv[i] -= sh0;
-      sv[i + 1] -= sh1;
-      sw[i] -= sh0;
-      sw[i + 1] -= sh1;
-    }
-  }
-  float p[8], r[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    p[i] = fast_exp2(sv[i]);
-    r[i] = fast_exp2(sw[i]);
-  }
-  bP[0][0] = movtrans(pack_h2(p[0], p[1]));
-  bP[0][1] = movtrans(pack_h2(p[2], p[3]));
-  bP[1][0] = movtrans(pack_h2(p[4], p[5]));
-  bP[1][1] = movtrans(pack_h2(p[6], p[7]));
-  bQ[0][0] = movtrans(pack_h2(r[0], r[1]));
-  bQ[0][1] = movtrans(pack_h2(r[2], r[3]));
-  bQ[1][0] = movtrans(pack_h2(r[4], r[5]));
-  bQ[1][1] = movtrans(pack_h2(r[6], r[7]));
-}
-
-template <int D>
-__device__ __forceinline__ void rescale_acc(Acc<D>& acc, float al0, float al1) {
-#pragma unroll
-  for (int m = 0; m < D / 16; ++m) {
-    acc.o[m][0] *= al0; acc.o[m][2] *= al0;
-    acc.o[m][1] *= al1; acc.o[m][3] *= al1;
-  }
-  acc.zs[0] *= al0; acc.zs[2] *= al0;
-  acc.zs[1] *= al1; acc.zs[3] *= al1;
-  acc.zs2[0] *= al0; acc.zs2[2] *= al0;
-  acc.zs2[1] *= al1; acc.zs2[3] *= al1;
-}
-
-template <int D>
-__device__ __forceinline__ void softmax_tile(float (&sv)[8], Softmax& st, Acc<D>& acc, uint32_t (&bP)[2][2]) {
-  float al0, al1;
-  bool resc;
-  softmax_p(sv, st, bP, al0, al1, resc);
-  if (resc) rescale_acc<D>(acc, al0, al1);
 }
 
 // Shared-memory vector load of NB bytes (2, 4, 8, 16 or a multiple of 16) into words.
@@ -373,10 +305,10 @@ struct QFrag {
 // 4g / 4g+1 (fields 0 / 1), M tile 1 = tokens 4g+2 / 4g+3.  PV k-step ks, lane q covers
 // tokens T0 = 8q + 2ks, T1 = T0 + 4 (a0) and T0+1, T1+1 (a2).
 template <int D, bool LO>
-__device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
-                                        int lane, const Softmax& st, float (&sv)[8]) {
+__device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
+                                          int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
-  constexpr int KB = D / 4, LB = KB < 16 ? KB : 16;
+  constexpr int KB = D / 4, NG = C::NGRP, LB = KB < 16 ? KB : 16;
   const int g = lane >> 2, q = lane & 3;
   uint32_t kw[C::NCH], ksw[2 * C::NCH], kzw[2 * C::NCH];
 #pragma unroll
@@ -413,22 +345,11 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
   }
   const float b0 = fmaf(cbE[0] + cbO[2], qscale, -st.m0), b1 = fmaf(cbE[1] + cbO[3], qscale, -st.m1);
   const float f0 = P24 * qscale, f1 = P22 * qscale, f2 = P20 * qscale, f3 = P18 * qscale;
-  sv[0] = fmaf(c0[0] + d0[0], f0, b0);
-  sv[1] = fmaf(c0[1] + d0[1], f0, b1);
-  sv[2] = fmaf(c0[2] + d0[2], f1, b0);
-  sv[3] = fmaf(c0[3] + d0[3], f1, b1);
-  sv[4] = fmaf(c1[0] + d1[0], f2, b0);
-  sv[5] = fmaf(c1[1] + d1[1], f2, b1);
-  sv[6] = fmaf(c1[2] + d1[2], f3, b0);
-  sv[7] = fmaf(c1[3] + d1[3], f3, b1);
-}
-
-template <int D>
-__device__ __forceinline__ void int2_pv(const uint8_t* __restrict__ buf, const uint32_t (&bP)[2][2], int lane,
-                                        Acc<D>& acc) {
-  using C = Cfg<D>;
-  constexpr int NG = C::NGRP;
-  const int g = lane >> 2, q = lane & 3;
+  float sv[8] = {fmaf(c0[0] + d0[0], f0, b0), fmaf(c0[1] + d0[1], f0, b1), fmaf(c0[2] + d0[2], f1, b0),
+                       fmaf(c0[3] + d0[3], f1, b1), fmaf(c1[0] + d1[0], f2, b0), fmaf(c1[1] + d1[1], f2, b1),
+                       fmaf(c1[2] + d1[2], f3, b0), fmaf(c1[3] + d1[3], f3, b1)};
+  uint32_t bP[2][2];
+  softmax_tile<D>(sv, st, acc, bP);
   // V params: one 16 B quad per (q, group j) = (ks0.p0, ks1.p0, ks0.p1, ks1.p1)
   uint32_t vs[4 * NG], vz[4];
 #pragma unroll
@@ -452,16 +373,6 @@ __device__ __forceinline__ void int2_pv(const uint8_t* __restrict__ buf, const u
   }
 }
 
-template <int D, bool LO>
-__device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
-                                          int lane, Softmax& st, Acc<D>& acc) {
-  float sv[8];
-  uint32_t bP[2][2];
-  int2_qk<D, LO>(buf, qf, qscale, lane, st, sv);
-  softmax_tile<D>(sv, st, acc, bP);
-  int2_pv<D>(buf, bP, lane, acc);
-}
-
 // ---------------------------------- INT4 slot tile ----------------------------------
 // Row -> slot map inside an M tile: rows 0-7 -> rho(r), rows 8-15 -> 8 + rho(r - 8) with
 // rho = [0,2,1,3,6,4,7,5]: QK K loads (lanes g = 2p, 2p+1 two slots apart) and PV V
@@ -470,12 +381,13 @@ __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const
 __device__ __forceinline__ int rho(int r) { return (0x57463120u >> (4 * r)) & 7; }
 
 template <int D, bool FULL, bool LO>
-__device__ __forceinline__ void int4_qk(const uint8_t* __restrict__ buf, int nv, const QFrag<D, LO>& qf,
-                                        float qscale, int lane, const Softmax& st, float (&sv)[8]) {
+__device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const QFrag<D, LO>& qf,
+                                          float qscale, int lane, Softmax& st, Acc<D>& acc) {
   using C = Cfg<D>;
   constexpr int S = C::SS, NG = C::NGRP;
   const int g = lane >> 2, q = lane & 3;
   const float fs = P24 * qscale;  // every INT4 K product is at 2^-24 (high-nibble q is pre-divided by 16)
+  float sv[8];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int sa = 16 * mt + rho(g), sb = sa + 8;
@@ -529,14 +441,8 @@ __device__ __forceinline__ void int4_qk(const uint8_t* __restrict__ buf, int nv,
     sv[4 * mt + 2] = tb0;
     sv[4 * mt + 3] = tb1;
   }
-}
-
-template <int D, bool FULL>
-__device__ __forceinline__ void int4_pv(const uint8_t* __restrict__ buf, int nv, const uint32_t (&bP)[2][2],
-                                        int lane, Acc<D>& acc) {
-  using C = Cfg<D>;
-  constexpr int S = C::SS, NG = C::NGRP;
-  const int g = lane >> 2, q = lane & 3;
+  uint32_t bP[2][2];
+  softmax_tile<D>(sv, st, acc, bP);
   // PV k-step ks: k = 2q, 2q+1, 2q+8, 2q+9 = rows of QK M tile ks -> slots ta, tb, tc, td
   constexpr int VB = 2 * NG;  // this lane's code bytes per token: 2 per group
   constexpr int VWN = VB < 4 ? 1 : VB / 4;
@@ -594,116 +500,6 @@ __device__ __forceinline__ void int4_pv(const uint8_t* __restrict__ buf, int nv,
   }
 }
 
-template <int D, bool FULL, bool LO>
-__device__ __forceinline__ void int4_tile(const uint8_t* __restrict__ buf, int nv, const QFrag<D, LO>& qf,
-                                          float qscale, int lane, Softmax& st, Acc<D>& acc) {
-  float sv[8];
-  uint32_t bP[2][2];
-  int4_qk<D, FULL, LO>(buf, nv, qf, qscale, lane, st, sv);
-  softmax_tile<D>(sv, st, acc, bP);
-  int4_pv<D, FULL>(buf, nv, bP, lane, acc);
-}
-
-// Tile metadata: the page id (INT2 tile) or this lane's INT4 index (INT4 tile).
-__device__ __forceinline__ int tile_meta(const DecodeArgs& a, const Unit& u, int t, int lane) {
-  if (t < u.npg) return a.page_ids[u.pg0 + t];
-  const int it = t - u.npg;
-  return lane < min(32, u.n4 - 32 * it) ? a.int4_ids[u.i40 + 32 * it + lane] : 0;
-}
-
-// TMA bulk copies of tile t into buf, completing on bar (whole warp calls): one 3 KB copy
-// per INT2 page, one copy per run of consecutive INT4 slots (fresh pools give long runs).
-template <int D>
-__device__ __forceinline__ void issue_tile(const Unit& u, int t, int meta, uint8_t* buf, uint64_t* bar, int lane,
-                                           const uint8_t* kv2, const uint8_t* kv4) {
-  using C = Cfg<D>;
-  if (t < u.npg) {
-    if (lane == 0) {
-      mbar_expect_tx(bar, C::PS);
-      bulk_g2s(buf, kv2 + (int64_t)meta * C::PS, C::PS, bar);
-    }
-  } else {
-    const int nv = min(32, u.n4 - 32 * (t - u.npg));
-    const int prev = __shfl_up_sync(0xffffffffu, meta, 1);
-    const bool start = lane < nv && (lane == 0 || meta != prev + 1);
-    const uint32_t starts = __ballot_sync(0xffffffffu, start);
-    if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
-    __syncwarp();
-    if (start) {
-      const uint32_t later = starts & ~((2u << lane) - 1u);
-      const int end = later ? __ffs(later) - 1 : nv;
-      bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)meta * C::SS, (end - lane) * C::SS, bar);
-    }
-  }
-}
-
-// One warp's (acc, zero sums) -> smem row block w of the piece merge: acc[h][c] = 2^(24-2e) O^T + zsum.
-template <int D>
-__device__ __forceinline__ void store_warp_acc(const Acc<D>& acc, float* sm_acc, int w, int lane) {
-  using C = Cfg<D>;
-  const int g = lane >> 2, q = lane & 3;
-  float z0[C::NGRP], z1[C::NGRP];  // sum_t p z of group j for heads 2q, 2q+1 (from lane (j, q))
-#pragma unroll
-  for (int j = 0; j < C::NGRP; ++j) {
-    z0[j] = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[2], 4 * j + q);
-    z1[j] = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[3], 4 * j + q);
-  }
-#pragma unroll
-  for (int m = 0; m < C::NCH; ++m) {
-    const int j = m >> 1;
-    const int ch0 = 32 * j + 4 * g + 2 * (m & 1);
-    // channel 4g + e of group j carries 2^(2e-24): e = 0/1 in even M tiles, 2/3 in odd ones
-    const float f0 = (m & 1) ? P20 : P24, f1 = (m & 1) ? P18 : P22;
-    sm_acc[(w * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, z0[j]);
-    sm_acc[(w * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, z1[j]);
-    sm_acc[(w * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, z0[j]);
-    sm_acc[(w * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(acc.o[m][3], f1, z1[j]);
-  }
-}
-
-// Q fragments of one unit (see QFrag) written by one warp into the CTA's smem table.
-template <int D, bool LO>
-__device__ __forceinline__ void build_qtab(const DecodeArgs& a, const Unit& u, uint64_t* qtab, int lane) {
-  using C = Cfg<D>;
-  using QF = QFrag<D, LO>;
-  const int g = lane >> 2, q = lane & 3;
-  const bool hv = g < a.gq;
-  const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
-  auto qv = [&](int c) { return hv ? load_q(a, qrow + c) : 0.f; };
-  auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
-  auto put = [&](int f, uint64_t v) { qtab[f * 32 + lane] = v; };
-#pragma unroll
-  for (int i = 0; i < C::NCH; ++i) {
-    const int cb = q * (D / 4) + 4 * i;
-    const float x0 = qv(cb), x1 = qv(cb + 1), x2 = qv(cb + 2), x3 = qv(cb + 3);
-    put(i, pack_b64(pack_h2(x0, x2), pack_h2(x1, x3)));
-    if constexpr (LO) put(2 * QF::NCH + 2 + i, pack_b64(pack_h2(lo(x0), lo(x2)), pack_h2(lo(x1), lo(x3))));
-  }
-  float qa = 0.f, qb = 0.f;  // Q_2q, Q_2q+1 (group sums, fp32)
-#pragma unroll
-  for (int j = 0; j < C::NGRP; ++j) {
-    const int cb = 32 * j + 8 * q;
-    float y[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) y[e] = qv(cb + e);
-    // high-nibble channels (cb+1, cb+5, cb+3, cb+7) enter at 2^-20: their q is divided by 16
-    constexpr float R16 = 0.0625f;
-    put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1] * R16, y[5] * R16), pack_h2(y[0], y[4])));
-    put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3] * R16, y[7] * R16)));
-    if constexpr (LO) {
-      put(3 * QF::NCH + 2 + 2 * j, pack_b64(pack_h2(lo(y[1]) * R16, lo(y[5]) * R16), pack_h2(lo(y[0]), lo(y[4]))));
-      put(3 * QF::NCH + 2 + 2 * j + 1, pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]) * R16, lo(y[7]) * R16)));
-    }
-    float part = ((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]));
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    if (j == 2 * q) qa = part;
-    if (j == 2 * q + 1) qb = part;
-  }
-  put(2 * QF::NCH, pack_b64(pack_h2(qa, qb), 0u));
-  put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
-}
-
 template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false>
 __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
@@ -732,27 +528,36 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
 
   // tile metadata: the page id (INT2 tile) or this lane's slot (INT4 tile); loaded one
   // iteration before its copy is issued so the copy never waits on the index load
-  // INT2 page ids come 32 tiles per coalesced load (lane i: this warp's tile 32b + i), the
-  // next batch prefetched; INT4 tiles load their 32 slot ids per tile.  k only increases.
-  int ids_cur = 0, ids_nxt = 0, batch_cur = -2;
-  auto load_ids = [&](int b) -> int {
-    const int kk = 32 * b + lane, t = u.tlo + warp + kk * NW;
-    return (kk < nmine && t < u.npg) ? a.page_ids[u.pg0 + t] : 0;
-  };
   auto load_meta = [&](int k) -> int {
     if (k >= nmine) return 0;
     const int t = u.tlo + warp + k * NW;
-    if (!KVMIX_BATCHIDS || t >= u.npg) return tile_meta(a, u, t, lane);
-    const int b = k >> 5;
-    if (b != batch_cur) {
-      ids_cur = (b == batch_cur + 1) ? ids_nxt : load_ids(b);
-      ids_nxt = load_ids(b + 1);
-      batch_cur = b;
-    }
-    return __shfl_sync(0xffffffffu, ids_cur, k & 31);
+    if (t < u.npg) return a.page_ids[u.pg0 + t];
+    const int it = t - u.npg;
+    return lane < min(32, u.n4 - 32 * it) ? a.int4_ids[u.i40 + 32 * it + lane] : 0;
   };
   auto issue = [&](int k, int meta, int s) {
-    issue_tile<D>(u, u.tlo + warp + k * NW, meta, ring + s * C::BUF, &bars[warp][s], lane, kv2, kv4);
+    const int t = u.tlo + warp + k * NW;
+    uint8_t* buf = ring + s * C::BUF;
+    uint64_t* bar = &bars[warp][s];
+    if (t < u.npg) {
+      if (lane == 0) {
+        mbar_expect_tx(bar, C::PS);
+        bulk_g2s(buf, kv2 + (int64_t)meta * C::PS, C::PS, bar);
+      }
+    } else {
+      // one bulk copy per run of consecutive INT4 slots (fresh pools give long runs)
+      const int nv = min(32, u.n4 - 32 * (t - u.npg));
+      const int prev = __shfl_up_sync(0xffffffffu, meta, 1);
+      const bool start = lane < nv && (lane == 0 || meta != prev + 1);
+      const uint32_t starts = __ballot_sync(0xffffffffu, start);
+      if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
+      __syncwarp();
+      if (start) {
+        const uint32_t later = starts & ~((2u << lane) - 1u);
+        const int end = later ? __ffs(later) - 1 : nv;
+        bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)meta * C::SS, (end - lane) * C::SS, bar);
+      }
+    }
   };
   if (MEMORY) {
     int s0 = stage;  // the ring continues where the previous piece left it
@@ -761,11 +566,50 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       if (++s0 == STAGES) s0 = 0;
     }
   }
-  int meta_next = load_meta(STAGES), meta_next2 = load_meta(STAGES + 1);  // metas run two tiles ahead
+  int meta_next = load_meta(STAGES);
 
   // ---- Q fragments (see QFrag): built once per CTA by warp 0 into shared memory ----
   uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + NW * STAGES * C::BUF);
-  if (warp == 0) build_qtab<D, LO>(a, u, qtab, lane);
+  if (warp == 0) {
+    const bool hv = g < a.gq;
+    const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
+    auto qv = [&](int c) { return hv ? load_q(a, qrow + c) : 0.f; };
+    auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
+    using QF = QFrag<D, LO>;
+    auto put = [&](int f, uint64_t v) { qtab[f * 32 + lane] = v; };
+#pragma unroll
+    for (int i = 0; i < C::NCH; ++i) {
+      const int cb = q * (D / 4) + 4 * i;
+      const float x0 = qv(cb), x1 = qv(cb + 1), x2 = qv(cb + 2), x3 = qv(cb + 3);
+      put(i, pack_b64(pack_h2(x0, x2), pack_h2(x1, x3)));
+      if constexpr (LO) put(2 * QF::NCH + 2 + i, pack_b64(pack_h2(lo(x0), lo(x2)), pack_h2(lo(x1), lo(x3))));
+    }
+    float qa = 0.f, qb = 0.f;  // Q_2q, Q_2q+1 (group sums, fp32)
+#pragma unroll
+    for (int j = 0; j < C::NGRP; ++j) {
+      const int cb = 32 * j + 8 * q;
+      float y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) y[e] = qv(cb + e);
+      // high-nibble channels (cb+1, cb+5, cb+3, cb+7) enter at 2^-20: their q is divided by 16
+      constexpr float R16 = 0.0625f;
+      put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1] * R16, y[5] * R16), pack_h2(y[0], y[4])));
+      put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3] * R16, y[7] * R16)));
+      if constexpr (LO) {
+        put(3 * QF::NCH + 2 + 2 * j,
+            pack_b64(pack_h2(lo(y[1]) * R16, lo(y[5]) * R16), pack_h2(lo(y[0]), lo(y[4]))));
+        put(3 * QF::NCH + 2 + 2 * j + 1,
+            pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]) * R16, lo(y[7]) * R16)));
+      }
+      float part = ((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]));
+      part += __shfl_xor_sync(0xffffffffu, part, 1);
+      part += __shfl_xor_sync(0xffffffffu, part, 2);
+      if (j == 2 * q) qa = part;
+      if (j == 2 * q + 1) qb = part;
+    }
+    put(2 * QF::NCH, pack_b64(pack_h2(qa, qb), 0u));
+    put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
+  }
   __syncthreads();
   const QFrag<D, LO> qf{qtab + lane};
 
@@ -776,75 +620,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
   Softmax st{0.f, 0.f, false};
 
-#if KVMIX_PAIRS
-  for (int k = 0; k < nmine;) {
-    const int t = u.tlo + warp + k * NW;
-    const uint8_t* buf = ring + stage * C::BUF;
-    const int stage2 = stage + 1 == STAGES ? 0 : stage + 1;
-    const uint32_t phase2 = stage + 1 == STAGES ? phase ^ 1u : phase;
-    // two same-bitwidth full tiles at once (64 tokens: more independent MMA chains, one vote)
-    const bool two = PAIRS && COMPUTE && k + 1 < nmine &&
-                     ((t + NW < u.npg) || (t >= u.npg && u.n4 - 32 * (t + NW - u.npg) >= 32));
-    if (MEMORY) mbar_wait(&bars[warp][stage], phase);
-    if (two) {
-      if (MEMORY) mbar_wait(&bars[warp][stage2], phase2);
-      const uint8_t* buf2 = ring + stage2 * C::BUF;
-      float sv[8], sw[8];
-      uint32_t bP[2][2], bQ[2][2];
-      float al0, al1;
-      bool resc;
-      if (t < u.npg) {
-        int2_qk<D, LO>(buf, qf, a.qscale, lane, st, sv);
-        int2_qk<D, LO>(buf2, qf, a.qscale, lane, st, sw);
-        softmax_p2(sv, sw, st, bP, bQ, al0, al1, resc);
-        if (resc) rescale_acc<D>(acc, al0, al1);
-        int2_pv<D>(buf, bP, lane, acc);
-        int2_pv<D>(buf2, bQ, lane, acc);
-      } else {
-        int4_qk<D, true, LO>(buf, 32, qf, a.qscale, lane, st, sv);
-        int4_qk<D, true, LO>(buf2, 32, qf, a.qscale, lane, st, sw);
-        softmax_p2(sv, sw, st, bP, bQ, al0, al1, resc);
-        if (resc) rescale_acc<D>(acc, al0, al1);
-        int4_pv<D, true>(buf, 32, bP, lane, acc);
-        int4_pv<D, true>(buf2, 32, bQ, lane, acc);
-      }
-    } else if (!COMPUTE) {
-      // measurement variant: data movement only (no dequant / MMA)
-    } else if (t < u.npg) {
-      int2_tile<D, LO>(buf, qf, a.qscale, lane, st, acc);
-    } else {
-      const int nv = min(32, u.n4 - 32 * (t - u.npg));
-      if (nv == 32) int4_tile<D, true, LO>(buf, 32, qf, a.qscale, lane, st, acc);
-      else int4_tile<D, false, LO>(buf, nv, qf, a.qscale, lane, st, acc);
-    }
-    __syncwarp();
-    const int nt = two ? 2 : 1;
-    for (int i = 0; i < nt; ++i) {
-      if (MEMORY && k + STAGES < nmine) {
-        fence_proxy_async();
-        issue(k + STAGES, meta_next, stage);
-      }
-      meta_next = meta_next2;
-      meta_next2 = load_meta(k + STAGES + 2);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
-      }
-      ++k;
-    }
-  }
-
-#else
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
     const uint8_t* buf = ring + stage * C::BUF;
     const int meta = meta_next;
-#if KVMIX_META2
-    meta_next = meta_next2;
-    meta_next2 = load_meta(k + STAGES + 2);
-#else
     meta_next = load_meta(k + STAGES + 1);
-#endif
     if (MEMORY) mbar_wait(&bars[warp][stage], phase);
     if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
@@ -865,7 +645,6 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
       phase ^= 1u;
     }
   }
-#endif
 
   // ---- finalize this warp: l per head from the ones rows, acc[h][c] = 2^(24-2e) O^T + zsum ----
   const float l0 = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[0], 28 + q);  // row 7 >= NG
@@ -874,7 +653,24 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   float* sm_acc = reinterpret_cast<float*>(smem);
   float* sm_m = sm_acc + NW * 8 * D;
   float* sm_l = sm_m + NW * 8;
-  store_warp_acc<D>(acc, sm_acc, warp, lane);
+  float z0[C::NGRP], z1[C::NGRP];  // sum_t p z of group j for heads 2q, 2q+1 (from lane (j, q))
+#pragma unroll
+  for (int j = 0; j < C::NGRP; ++j) {
+    z0[j] = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[2], 4 * j + q);
+    z1[j] = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[3], 4 * j + q);
+  }
+#pragma unroll
+  for (int m = 0; m < C::NCH; ++m) {
+    const int j = m >> 1;
+    const int e0 = 2 * (m & 1);
+    const int ch0 = 32 * j + 4 * g + e0;
+    // channel 4g + e of group j carries 2^(2e-24): e = 0/1 in even M tiles, 2/3 in odd ones
+    const float f0 = (m & 1) ? P20 : P24, f1 = (m & 1) ? P18 : P22;
+    sm_acc[(warp * 8 + 2 * q) * D + ch0] = fmaf(acc.o[m][0], f0, z0[j]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0] = fmaf(acc.o[m][1], f0, z1[j]);
+    sm_acc[(warp * 8 + 2 * q) * D + ch0 + 1] = fmaf(acc.o[m][2], f1, z0[j]);
+    sm_acc[(warp * 8 + 2 * q + 1) * D + ch0 + 1] = fmaf(acc.o[m][3], f1, z1[j]);
+  }
   if (g == 0) {
     sm_m[warp * 8 + 2 * q] = st.init ? st.m0 : -INFINITY;  // a warp without tiles contributes nothing
     sm_m[warp * 8 + 2 * q + 1] = st.init ? st.m1 : -INFINITY;
@@ -883,158 +679,6 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   }
   finish_piece<D>(a, u, sm_m, sm_l, sm_acc, &sm_flag);
   __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
-  }
-}
-
-// ====================================================================================
-// Variant 4: warp-specialised tensor-core kernel.  A CTA holds NPAIR pairs of warps; in
-// pair p, warp p (QK) issues the TMA copies of the pair's tiles and computes the logits
-// S = QK^T (dequantised in registers), handing them (32 B per lane) to warp p + NPAIR (PV)
-// through the tile's own ring slot; the PV warp runs the online softmax and owns the
-// running max and the O / zero-point / softmax-sum accumulators.  The two halves of a
-// tile overlap across tiles, and each warp's dependency chains are half as long as in the
-// fused kernel.  Slot life: TMA (full) -> QK publishes S (pready) -> PV done (empty).
-#ifndef KVMIX_WS_STAGES
-#define KVMIX_WS_STAGES 4
-#endif
-#ifndef KVMIX_WS_MINB
-#define KVMIX_WS_MINB 2
-#endif
-constexpr int NPAIR = NW;                 // warp pairs per CTA (the merge treats pairs like warps)
-constexpr int WSTAGES = KVMIX_WS_STAGES;  // ring slots per pair; the QK warp prefetches WSTAGES - 2 tiles
-constexpr int PAREA = 1024;               // per slot: the tile's logits S (32 lanes x 8 fp32)
-
-template <int D>
-struct WsCfg {
-  static constexpr int SLOT = Cfg<D>::BUF + PAREA;
-  static constexpr int RING = NPAIR * WSTAGES * SLOT;
-  static constexpr int SMEM = RING + (D / 8 + 2) * 32 * 8 * 2;  // rings + q fragment table (LO size)
-};
-
-template <int D, bool LO>
-__global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kernel(const DecodeArgs a) {
-  using C = Cfg<D>;
-  using W = WsCfg<D>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[NPAIR][WSTAGES], pready[NPAIR][WSTAGES], empty[NPAIR][WSTAGES];
-  __shared__ float sm_m[NPAIR * 8], sm_l[NPAIR * 8];
-  __shared__ int sm_flag;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int g = lane >> 2, q = lane & 3;
-  const bool is_qk = warp < NPAIR;
-  const int pair = is_qk ? warp : warp - NPAIR;
-  uint8_t* ring = smem + pair * WSTAGES * W::SLOT;
-  uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + W::RING);
-  if (threadIdx.x == 0) {
-    for (int p = 0; p < NPAIR; ++p)
-      for (int s = 0; s < WSTAGES; ++s) {
-        mbar_init(&full[p][s], 1);
-        mbar_init(&pready[p][s], 1);
-        mbar_init(&empty[p][s], 1);
-      }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  uint32_t kg = 0;  // tiles this pair has run so far (both warps count identically)
-
-  for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
-    const Unit u = load_unit(a, piece);
-    const int ntiles = u.thi - u.tlo;
-    const int nmine = ntiles > pair ? (ntiles - pair + NPAIR - 1) / NPAIR : 0;
-    auto tile_of = [&](int k) { return u.tlo + pair + k * NPAIR; };
-    if (warp == 0) build_qtab<D, LO>(a, u, qtab, lane);
-    __syncthreads();
-
-    if (is_qk) {
-      const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
-      const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
-      auto meta_of = [&](int k) { return k < nmine ? tile_meta(a, u, tile_of(k), lane) : 0; };
-      auto do_issue = [&](int k, int meta) {  // tile k of this piece; its slot must be released by the PV warp
-        const uint32_t gk = kg + k;
-        const int s = gk % WSTAGES;
-        if (gk >= WSTAGES) mbar_wait(&empty[pair][s], ((gk / WSTAGES) - 1) & 1);
-        issue_tile<D>(u, tile_of(k), meta, ring + s * W::SLOT, &full[pair][s], lane, kv2, kv4);
-      };
-      for (int k = 0; k < WSTAGES - 2 && k < nmine; ++k) do_issue(k, meta_of(k));
-      int meta_next = meta_of(WSTAGES - 2);  // index loads run one tile ahead of their copies
-      const QFrag<D, LO> qf{qtab + lane};
-      const Softmax s0{0.f, 0.f, false};  // the QK warp emits unshifted logits; the PV warp owns the max
-      for (int k = 0; k < nmine; ++k) {
-        const uint32_t gk = kg + k;
-        const int s = gk % WSTAGES;
-        uint8_t* buf = ring + s * W::SLOT;
-        mbar_wait(&full[pair][s], (gk / WSTAGES) & 1);
-        const int t = tile_of(k);
-        float sv[8];
-        if (t < u.npg) {
-          int2_qk<D, LO>(buf, qf, a.qscale, lane, s0, sv);
-        } else {
-          const int nv = min(32, u.n4 - 32 * (t - u.npg));
-          if (nv == 32) int4_qk<D, true, LO>(buf, 32, qf, a.qscale, lane, s0, sv);
-          else int4_qk<D, false, LO>(buf, nv, qf, a.qscale, lane, s0, sv);
-        }
-        float4* sa = reinterpret_cast<float4*>(buf + C::BUF) + 2 * lane;
-        sa[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
-        sa[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pready[pair][s]);
-        if (k + WSTAGES - 2 < nmine) {
-          const int meta = meta_next;
-          meta_next = meta_of(k + WSTAGES - 1);
-          do_issue(k + WSTAGES - 2, meta);
-        }
-      }
-      kg += nmine;
-      __syncthreads();  // (A) every pair has finished the piece: the rings are idle
-      __syncthreads();  // (B) PV warps have written the merge scratch
-    } else {
-      Acc<D> acc;
-#pragma unroll
-      for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
-      acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
-      acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
-      Softmax st{0.f, 0.f, false};
-      for (int k = 0; k < nmine; ++k) {
-        const uint32_t gk = kg + k;
-        const int s = gk % WSTAGES;
-        const uint8_t* buf = ring + s * W::SLOT;
-        const uint32_t ph = (gk / WSTAGES) & 1;
-        mbar_wait(&pready[pair][s], ph);
-        mbar_wait(&full[pair][s], ph);  // already complete; makes the TMA bytes visible to this warp
-        const float4* sa = reinterpret_cast<const float4*>(buf + C::BUF) + 2 * lane;
-        const float4 x0 = sa[0], x1 = sa[1];
-        float sv[8] = {x0.x - st.m0, x0.y - st.m1, x0.z - st.m0, x0.w - st.m1,
-                       x1.x - st.m0, x1.y - st.m1, x1.z - st.m0, x1.w - st.m1};
-        uint32_t bP[2][2];
-        softmax_tile<D>(sv, st, acc, bP);
-        const int t = tile_of(k);
-        if (t < u.npg) {
-          int2_pv<D>(buf, bP, lane, acc);
-        } else {
-          const int nv = min(32, u.n4 - 32 * (t - u.npg));
-          if (nv == 32) int4_pv<D, true>(buf, 32, bP, lane, acc);
-          else int4_pv<D, false>(buf, nv, bP, lane, acc);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[pair][s]);
-      }
-      if (g == 0) {
-        sm_m[pair * 8 + 2 * q] = st.init ? st.m0 : -INFINITY;  // a pair without tiles contributes nothing
-        sm_m[pair * 8 + 2 * q + 1] = st.init ? st.m1 : -INFINITY;
-      }
-      const float l0 = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[0], 28 + q);  // ones rows (row 7)
-      const float l1 = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[1], 28 + q);
-      kg += nmine;
-      __syncthreads();  // (A)
-      store_warp_acc<D>(acc, reinterpret_cast<float*>(smem), pair, lane);
-      if (g == 0) {
-        sm_l[pair * 8 + 2 * q] = l0;
-        sm_l[pair * 8 + 2 * q + 1] = l1;
-      }
-      __syncthreads();  // (B)
-    }
-    finish_piece<D>(a, u, sm_m, sm_l, reinterpret_cast<const float*>(smem), &sm_flag);
-    __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
   }
 }
 
@@ -1127,12 +771,12 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
 }
 
 template <typename Kern>
-static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_cta, int smem, cudaStream_t s, int nwarps = NW) {
+static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_cta, int smem, cudaStream_t s) {
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
   }
-  kern<<<(unsigned)n_cta, nwarps * 32, smem, s>>>(a);
+  kern<<<(unsigned)n_cta, NW * 32, smem, s>>>(a);
   return check_launch("flash_decode");
 }
 
@@ -1143,13 +787,9 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
       // fp32 q carries bits fp16 cannot hold: add the q - fp16(q) correction MMAs
       if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_mma_kernel<D, true, true, true>, a, n_work, Cfg<D>::SMEM, s);
       return launch_kernel(decode_mma_kernel<D, true, true, false>, a, n_work, Cfg<D>::SMEM, s);
-    case 4:
-      if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_ws_kernel<D, true>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
-      return launch_kernel(decode_ws_kernel<D, false>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
     case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, 0, s);
     case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
-    case 3: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
-    default: return fail(KVMIX_EINVAL, "bad variant");
+    default: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
   }
 }
 
@@ -1191,7 +831,7 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   if (batch <= 0 || n_cta <= 0 || n_cta > (1 << 20)) return fail(KVMIX_EINVAL, "empty batch or CTA schedule");
   if (!work || !cta_ptr || !counters) return fail(KVMIX_EINVAL, "work, cta_ptr and counters are required");
   if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
-  if (variant < 0 || variant > 4) return fail(KVMIX_EINVAL, "bad variant");
+  if (variant < 0 || variant > 3) return fail(KVMIX_EINVAL, "bad variant");
   DecodeArgs a;
   a.q = q;
   a.q_dtype = q_dtype;

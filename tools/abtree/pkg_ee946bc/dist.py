@@ -1,0 +1,104 @@
+"""Multi-GPU sharding of the decode hot path (one process per GPU, torch.distributed).
+
+The reference is single-process; the path shards two ways (8(e)):
+
+* batch-parallel (cfg5): requests -> ranks.  Every rank owns a full pool and its own
+  requests; there is no collective on the data path (weak scaling).
+* KV-head-parallel (cfg4): rank r owns KV heads [r*Hkv/W, (r+1)*Hkv/W) and their GQA
+  q heads.  Slot addresses are head-agnostic (blocks are keyed (slot, layer, head),
+  pool.py:108-110), so page tables are replicated: rank 0 runs the allocator and
+  broadcasts the slot lists, every rank quantizes only its head slice into its own
+  pool, decodes its heads, and one all-gather per layer assembles out [B, Hq, d].
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .errors import ValidationError
+
+
+def world() -> tuple[int, int]:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def shard_requests(request_ids, rank: int, world_size: int) -> list:
+    """Batch-parallel: contiguous, near-equal shards of the request list."""
+    n = len(request_ids)
+    lo = n * rank // world_size
+    hi = n * (rank + 1) // world_size
+    return list(request_ids[lo:hi])
+
+
+def head_slice(n_kv_heads: int, n_q_heads: int, rank: int, world_size: int) -> tuple[slice, slice]:
+    """KV-head-parallel: (kv head slice, q head slice) owned by ``rank``."""
+    if n_kv_heads % world_size:
+        raise ValidationError(f"{n_kv_heads} kv heads do not split over {world_size} ranks")
+    hk = n_kv_heads // world_size
+    g = n_q_heads // n_kv_heads
+    return slice(rank * hk, (rank + 1) * hk), slice(rank * hk * g, (rank + 1) * hk * g)
+
+
+def broadcast_slots(slots: np.ndarray | None, src: int = 0, group=None) -> np.ndarray:
+    """Replicate one request's slot list (page table) from ``src`` to every rank."""
+    rank, _ = world()
+    obj = [slots.tolist() if rank == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return np.asarray(obj[0], dtype=np.int64)
+
+
+def adopt_table(pool, request_id: str, slots: np.ndarray, partitioned: bool = False):
+    """Install a page table computed on another rank into this rank's pool (same
+    allocator state transition as ``alloc`` produced there)."""
+    from .pool import PageTable
+
+    cfg, g = pool.config, pool.config.page_size
+    if request_id in pool._tables:
+        raise ValidationError(f"request {request_id!r} already live")
+    slots = np.asarray(slots, dtype=np.int64)
+    pages = np.unique(slots[slots < cfg.offset] // g * g)
+    int4 = slots[slots >= cfg.offset]
+    free_pages = set(pool._free_pages)
+    free_int4 = set(pool._free_int4)
+    if not set(pages.tolist()) <= free_pages or not set(int4.tolist()) <= free_int4:
+        raise ValidationError("adopted table uses slots that are not free on this rank")
+    pool._free_pages = [p for p in pool._free_pages if p not in set(pages.tolist())]
+    pool._free_int4 = [s for s in pool._free_int4 if s not in set(int4.tolist())]
+    rix = pool._next_rid
+    pool._next_rid += 1
+    pool._rid_index[request_id] = rix
+    pool._owner[slots] = rix
+    table = PageTable(request_id=request_id, slots=slots, partitioned=partitioned)
+    pool._tables[request_id] = table
+    return table
+
+
+def gather_heads(out_local: torch.Tensor, out_full: torch.Tensor | None = None, group=None) -> torch.Tensor:
+    """All-gather the per-rank head slices [B, Hq/W, d] into [B, Hq, d] (rank-major
+    head order == natural head order because every rank owns a contiguous slice)."""
+    rank, W = world()
+    B, hl, d = out_local.shape
+    buf = torch.empty((W * B, hl, d), dtype=out_local.dtype, device=out_local.device)
+    if W == 1:
+        buf.copy_(out_local)
+    else:
+        dist.all_gather_into_tensor(buf, out_local.contiguous(), group=group)
+    full = buf.view(W, B, hl, d).permute(1, 0, 2, 3).reshape(B, W * hl, d)
+    if out_full is not None:
+        out_full.copy_(full)
+        return out_full
+    return full
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Timing is reported as the max over ranks (slowest rank defines the step)."""
+    rank, W = world()
+    if W == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
