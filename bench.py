@@ -431,14 +431,9 @@ def run_ours(args):
     if not args.no_e2e:
         q_host = q.cpu().pin_memory()
         o_host = torch.empty_like(q_host).pin_memory()
-        q_dev = torch.empty_like(q)
-        o_dev = torch.empty_like(q)
 
-        def e2e_step():
-            q_dev.copy_(q_host, non_blocking=True)
-            for layer in range(L):
-                kv.flash_decode_batched(q_dev[layer], batch, layer, out=o_dev[layer])
-            o_host.copy_(o_dev, non_blocking=True)
+        def e2e_step():  # public API: q in pinned host memory, outputs back to pinned host memory
+            kv.flash_decode_layers_from_host(q_host, batch, o_host)
 
         for _ in range(2):
             e2e_step()

@@ -13,6 +13,7 @@ from .attention import (
     SplitPartial,
     flash_decode,
     flash_decode_batched,
+    flash_decode_layers_from_host,
     merge_partials,
 )
 from .errors import CapacityError, InfeasibleBudgetError, KvmixError, TemplateStructureError, ValidationError

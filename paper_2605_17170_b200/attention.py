@@ -144,6 +144,55 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
     return out
 
 
+def flash_decode_layers_from_host(q_host: torch.Tensor, batch: DecodeBatch, out_host: torch.Tensor,
+                                  chunk: int = 8, scale: float | None = None) -> torch.Tensor:
+    """One decode step for all layers with q and the outputs on the HOST.
+
+    q_host, out_host: pinned [L, B, n_q_heads, d].  The layers run in chunks: the
+    host->device copy of chunk c+1 and the device->host copy of chunk c-1 overlap the
+    kernels of chunk c (two side copy streams, events between the streams).  Asynchronous
+    on the current stream: it returns once everything is enqueued and the current
+    stream is ordered after the last device->host copy.
+    """
+    pool, cfg = batch.pool, batch.pool.config
+    L = q_host.shape[0]
+    if tuple(q_host.shape[1:]) != (batch.batch, batch.n_q_heads, cfg.head_dim) or L > cfg.n_layers:
+        raise ValidationError(f"q_host must be [L <= {cfg.n_layers}, {batch.batch}, {batch.n_q_heads}, {cfg.head_dim}]")
+    if out_host.shape != q_host.shape:
+        raise ValidationError("out_host must match q_host")
+    dev = pool.device
+    st = getattr(batch, "_host_io", None)
+    if st is None or st["q"].shape != q_host.shape or st["q"].dtype != q_host.dtype:
+        st = {"q": torch.empty(q_host.shape, dtype=q_host.dtype, device=dev),
+              "o": torch.empty(out_host.shape, dtype=out_host.dtype, device=dev),
+              "h2d": torch.cuda.Stream(device=dev), "d2h": torch.cuda.Stream(device=dev)}
+        batch._host_io = st
+    qd, od, hs, ds = st["q"], st["o"], st["h2d"], st["d2h"]
+    compute = torch.cuda.current_stream(dev)
+    hs.wait_stream(compute)  # the previous step's kernels are done with qd / od
+    ds.wait_stream(compute)
+    chunks = [(c0, min(L, c0 + chunk)) for c0 in range(0, L, chunk)]
+    ev_in = []
+    with torch.cuda.stream(hs):  # every input chunk streams in up front, in order
+        for c0, c1 in chunks:
+            qd[c0:c1].copy_(q_host[c0:c1], non_blocking=True)
+            ev_in.append(torch.cuda.Event())
+            ev_in[-1].record(hs)
+    for (c0, c1), ev in zip(chunks, ev_in):
+        compute.wait_event(ev)
+        for layer in range(c0, c1):
+            flash_decode_batched(qd[layer], batch, layer, out=od[layer], scale=scale)
+        ev_out = torch.cuda.Event()
+        ev_out.record(compute)
+        ds.wait_event(ev_out)
+        with torch.cuda.stream(ds):  # a chunk's outputs leave while the next chunk computes
+            out_host[c0:c1].copy_(od[c0:c1], non_blocking=True)
+    compute.wait_stream(hs)
+    cs = ds
+    compute.wait_stream(cs)
+    return out_host
+
+
 def flash_decode(q, page_table, pool_view, split_len: int = 128, scale=None, variant: int = VARIANT_TENSOR_CORE):
     """attention.py:175-218 drop-in: single-query decode over a partitioned page table.
 
