@@ -60,7 +60,9 @@ struct Cfg {
   static constexpr int PS = page_stride(D);
   static constexpr int SS = slot_stride(D);
   static constexpr int BUF = PS > 32 * SS ? PS : 32 * SS;  // one INT2 page or 32 INT4 slots (slot-contiguous)
-  static constexpr int SMEM = NW * STAGES * BUF + (D / 8 + 2) * 32 * 8 * 2;  // ring + q fragment table (LO size)
+  static constexpr int QTAB = (D / 8 + 2) * 32 * 8 * 2;         // q fragment table (LO size)
+  static constexpr int MERGE = (NW * 8 * D + 2 * NW * 8) * 4;     // per-warp (acc, m, l) for the piece merge
+  static constexpr int SMEM = NW * STAGES * BUF + QTAB + MERGE;
 };
 
 struct DecodeArgs {
@@ -704,6 +706,25 @@ __device__ __forceinline__ void build_qtab(const DecodeArgs& a, const Unit& u, u
   put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
 }
 
+// Issue this warp's first STAGES tiles of piece u into its ring, starting at `stage`.
+template <int D>
+__device__ __forceinline__ void prime_piece(const DecodeArgs& a, const Unit& u, int warp, int lane, uint8_t* ring,
+                                            uint64_t (*bars)[STAGES], int stage) {
+  using C = Cfg<D>;
+  const int ntiles = u.thi - u.tlo;
+  const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
+  const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
+  const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
+  __syncwarp();
+  fence_proxy_async();  // the slots were last read through the generic proxy
+  int s0 = stage;
+  for (int k = 0; k < STAGES && k < nmine; ++k) {
+    const int t = u.tlo + warp + k * NW;
+    issue_tile<D>(u, t, tile_meta(a, u, t, lane), ring + s0 * C::BUF, &bars[warp][s0], lane, kv2, kv4);
+    if (++s0 == STAGES) s0 = 0;
+  }
+}
+
 template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false>
 __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
@@ -723,7 +744,9 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   int stage = 0;  // ring position and mbarrier phase persist across pieces
   uint32_t phase = 0;
 
-  for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
+  const int piece_end = a.cta_ptr[blockIdx.x + 1];
+  bool primed = false;  // the piece's first tiles were issued while the previous piece merged
+  for (int piece = a.cta_ptr[blockIdx.x]; piece < piece_end; ++piece) {
   const Unit u = load_unit(a, piece);
   const int ntiles = u.thi - u.tlo;
   const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
@@ -754,13 +777,14 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   auto issue = [&](int k, int meta, int s) {
     issue_tile<D>(u, u.tlo + warp + k * NW, meta, ring + s * C::BUF, &bars[warp][s], lane, kv2, kv4);
   };
-  if (MEMORY) {
+  if (MEMORY && !primed) {
     int s0 = stage;  // the ring continues where the previous piece left it
     for (int k = 0; k < STAGES && k < nmine; ++k) {
       issue(k, load_meta(k), s0);
       if (++s0 == STAGES) s0 = 0;
     }
   }
+  primed = false;
   int meta_next = load_meta(STAGES), meta_next2 = load_meta(STAGES + 1);  // metas run two tiles ahead
 
   // ---- Q fragments (see QFrag): built once per CTA by warp 0 into shared memory ----
@@ -867,11 +891,16 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
   }
 #endif
 
+  // ---- the next piece's first tiles stream in while this one merges (the ring is idle) ----
+  if (MEMORY && piece + 1 < piece_end) {
+    prime_piece<D>(a, load_unit(a, piece + 1), warp, lane, ring, bars, stage);
+    primed = true;
+  }
   // ---- finalize this warp: l per head from the ones rows, acc[h][c] = 2^(24-2e) O^T + zsum ----
   const float l0 = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[0], 28 + q);  // row 7 >= NG
   const float l1 = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[1], 28 + q);
-  __syncthreads();  // all warps done with their rings -> reuse ring smem for the merge
-  float* sm_acc = reinterpret_cast<float*>(smem);
+  __syncthreads();  // every warp is done with the q table and the previous merge scratch
+  float* sm_acc = reinterpret_cast<float*>(smem + NW * STAGES * C::BUF + C::QTAB);
   float* sm_m = sm_acc + NW * 8 * D;
   float* sm_l = sm_m + NW * 8;
   store_warp_acc<D>(acc, sm_acc, warp, lane);
