@@ -379,15 +379,23 @@ __device__ __forceinline__ void encode_group(const float (&x)[G], uint32_t (&w)[
   // element (the usual case: zero and scale round the true min / range by < 2^-11).
   const bool noclip = quot(mn) >= -0.5f && quot(mx) < (float)LEVELS + 0.5f;
   if (noclip) {
+    // codes enter the word by word = word * 2^BITS + bits(MAGIC + code) (one IMAD each, highest
+    // code first); the MAGIC bit patterns add up to a constant, removed once per word
+    constexpr uint32_t MB = 0x4B400000u;
+    constexpr uint32_t OFF = [] {
+      uint32_t o = 0u;
+      for (int i = 0; i < 32 / BITS; ++i) o = o * (1u << BITS) + MB;
+      return o;
+    }();
 #pragma unroll
     for (int k = 0; k < BITS; ++k) {
       uint32_t word = 0u;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) {
+      for (int i = PER - 1; i >= 0; --i) {
         const float a = __fadd_rn(quot(x[PER * k + i]), 0.5f);
-        word |= (__float_as_uint(__fadd_rd(a, MAGIC)) & (uint32_t)LEVELS) << (BITS * i);
+        word = word * (1u << BITS) + __float_as_uint(__fadd_rd(a, MAGIC));
       }
-      w[k] = word;
+      w[k] = word - OFF;
     }
   } else {
 #pragma unroll
