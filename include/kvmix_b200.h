@@ -134,6 +134,20 @@ int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dt
                        const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
                        float* partials, int32_t* counters, float scale, int32_t variant, void* stream);
 
+/* K4 fused decode append (pool.py:284-306 append_decode_token data half + attention.py:175
+ * flash_decode, one launch): the same as kvmix_flash_decode (variant 0) for one layer, where
+ * the host has already popped one INT4 slot per request and appended it to the table (the
+ * last entry of int4_ids of each request).  The warp that owns that slot's tile quantizes
+ * k_new / v_new [batch][n_kv_heads][d] (kv_dtype) into the tile it is about to read and into
+ * int4_pool, so the new token is both stored and attended to. */
+int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* out, int32_t out_dtype, uint8_t* int2_pool,
+                              uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
+                              int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
+                              const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
+                              const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
+                              float* partials, int32_t* counters, float scale, const void* k_new, const void* v_new,
+                              int32_t kv_dtype, void* stream);
+
 /* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
  * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */
 int kvmix_merge_partials(const float* acc, const float* lse, const float* max_logit, int64_t n, int64_t d, float* out,

@@ -105,6 +105,10 @@ class DecodeBatch:
         self.partials = torch.empty(max(1, n_parts) * 8 * (cfg.head_dim + 2), dtype=torch.float32, device=dev)
         self.counters = torch.zeros(self.batch * cfg.n_kv_heads, dtype=torch.int32, device=dev)
         self.n_tokens = t["n_pages"] * cfg.page_size + t["n_int4"]
+        # newest INT4 slot of each request (the fused decode append's target), host side
+        self.last_int4 = None
+        if self.request_ids is not None and np.all(t["n_int4"] > 0):
+            self.last_int4 = np.array([int(pool.table(r).slots[-1]) for r in self.request_ids], dtype=np.int64)
 
     def kv_bytes(self) -> int:
         """Algorithmic KV bytes one layer's decode reads (all kv heads)."""
@@ -116,11 +120,18 @@ class DecodeBatch:
 
 
 def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: torch.Tensor | None = None,
-                         scale: float | None = None, variant: int = VARIANT_TENSOR_CORE) -> torch.Tensor:
+                         scale: float | None = None, variant: int = VARIANT_TENSOR_CORE,
+                         append: tuple | None = None) -> torch.Tensor:
     """Decode attention for every request of ``batch`` at ``layer``.
 
     q: [B, n_q_heads, d] device tensor (f32/bf16/f16); returns out [B, n_q_heads, d]
     (dtype of q unless ``out`` is given).  Asynchronous on the current stream.
+
+    append=(k_new, v_new), each [B, n_kv_heads, d] on the device: the K4 fused decode append.
+    The newest INT4 slot of every request (reserved with ``pool.reserve_decode_slots`` before
+    ``batch.refresh()``) receives this layer's k/v, quantized inside the attention kernel
+    by the warp that reads it, and the new token is attended to (pool.py:284-306 followed by
+    attention.py:175-218, in one launch).
     """
     pool, cfg = batch.pool, batch.pool.config
     if q.dim() != 3 or q.shape[0] != batch.batch or q.shape[1] != batch.n_q_heads or q.shape[2] != cfg.head_dim:
@@ -134,6 +145,27 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
     if scale is None:
         scale = 1.0 / math.sqrt(cfg.head_dim)
     t = batch.csr
+    if append is not None:
+        k_new, v_new = append
+        want = (batch.batch, cfg.n_kv_heads, cfg.head_dim)
+        if tuple(k_new.shape) != want or tuple(v_new.shape) != want:
+            raise ValidationError(f"append k/v must be {want}")
+        if variant != VARIANT_TENSOR_CORE:
+            raise ValidationError("the fused decode append runs in the tensor-core kernel")
+        if np.any(t["n_int4"] == 0):
+            raise ValidationError("every request needs a reserved INT4 slot for the fused append")
+        k_new = k_new.contiguous()
+        v_new = v_new.to(k_new.dtype).contiguous()
+        _lib.check(lib.kvmix_flash_decode_append(
+            q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
+            pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,
+            batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
+            t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
+            batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), k_new.data_ptr(),
+            v_new.data_ptr(), _lib.dtype_code(k_new), _lib.stream()))
+        if batch.last_int4 is not None:
+            pool._int4_written[layer, :, batch.last_int4 - cfg.offset] = True
+        return out
     _lib.check(lib.kvmix_flash_decode(
         q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
         pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,

@@ -83,6 +83,13 @@ struct DecodeArgs {
   float* part;             // split partials [n_parts][8][D + 2] (acc[D], m, l; log2 domain)
   int32_t* counters;       // [batch * n_kv] arrival counters, zero between launches
   float qscale;            // softmax scale * log2(e)
+  // K4 fused decode append (variant 0): each request's newest token -- the last INT4 entry of
+  // its table -- is quantized from app_k / app_v [batch][n_kv][D] (app_dtype) by the warp
+  // that owns its tile, into that tile's staged record and into the pool (int4_pool_w).
+  const void* app_k;
+  const void* app_v;
+  int app_dtype;
+  uint8_t* int4_pool_w;
 };
 
 __device__ __forceinline__ float load_q(const DecodeArgs& a, int64_t idx) {
@@ -706,6 +713,25 @@ __device__ __forceinline__ void build_qtab(const DecodeArgs& a, const Unit& u, u
   put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
 }
 
+// K4 fused decode append, cold path (out of line): channel group j of the request's newest
+// token -> the staged slot record srec and its place in the pool.
+template <int D>
+__device__ __noinline__ void append_group(const DecodeArgs& a, const Unit& u, uint8_t* srec, int j) {
+  using C = Cfg<D>;
+  const int64_t slot = a.int4_ids[u.i40 + u.n4 - 1];
+  uint8_t* grec = a.int4_pool_w + ((a.layer * a.n_kv + u.kvh) * a.pool_int4 + slot) * (int64_t)C::SS;
+  const int64_t off = ((int64_t)u.b * a.n_kv + u.kvh) * D + 32 * j;
+  if (a.app_dtype == KVMIX_BF16)
+    encode_int4_group<D, __nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(a.app_k) + off,
+                                        reinterpret_cast<const __nv_bfloat16*>(a.app_v) + off, srec, grec, j, nullptr);
+  else if (a.app_dtype == KVMIX_F16)
+    encode_int4_group<D, __half>(reinterpret_cast<const __half*>(a.app_k) + off,
+                                 reinterpret_cast<const __half*>(a.app_v) + off, srec, grec, j, nullptr);
+  else
+    encode_int4_group<D, float>(reinterpret_cast<const float*>(a.app_k) + off,
+                                reinterpret_cast<const float*>(a.app_v) + off, srec, grec, j, nullptr);
+}
+
 // Issue this warp's first STAGES tiles of piece u into its ring, starting at `stage`.
 template <int D>
 __device__ __forceinline__ void prime_piece(const DecodeArgs& a, const Unit& u, int warp, int lane, uint8_t* ring,
@@ -725,7 +751,7 @@ __device__ __forceinline__ void prime_piece(const DecodeArgs& a, const Unit& u, 
   }
 }
 
-template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false>
+template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false, bool APPEND = false>
 __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -870,6 +896,11 @@ __global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const D
     meta_next = load_meta(k + STAGES + 1);
 #endif
     if (MEMORY) mbar_wait(&bars[warp][stage], phase);
+    if (APPEND && u.n4 > 0 && t == u.npg + (u.n4 - 1) / 32) {
+      // K4 fused: quantize the newest token over the stale copy the TMA brought in
+      if (lane < C::NGRP) append_group<D>(a, u, ring + stage * C::BUF + ((u.n4 - 1) % 32) * C::SS, lane);
+      __syncwarp();
+    }
     if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
     } else if (t < u.npg) {
@@ -1170,6 +1201,11 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
   switch (variant) {
     case 0:
       // fp32 q carries bits fp16 cannot hold: add the q - fp16(q) correction MMAs
+      if (a.app_k != nullptr) {  // K4 fused decode append
+        if (a.q_dtype == KVMIX_F32)
+          return launch_kernel(decode_mma_kernel<D, true, true, true, true>, a, n_work, Cfg<D>::SMEM, s);
+        return launch_kernel(decode_mma_kernel<D, true, true, false, true>, a, n_work, Cfg<D>::SMEM, s);
+      }
       if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_mma_kernel<D, true, true, true>, a, n_work, Cfg<D>::SMEM, s);
       return launch_kernel(decode_mma_kernel<D, true, true, false>, a, n_work, Cfg<D>::SMEM, s);
     case 4:
@@ -1207,13 +1243,13 @@ extern "C" int kvmix_merge_partials(const float* acc, const float* lse, const fl
   return check_launch("merge_partials");
 }
 
-extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
-                                  const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
-                                  int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
-                                  int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
-                                  const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
-                                  const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
-                                  float scale, int32_t variant, void* stream) {
+static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
+                             const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4,
+                             int64_t layer, int64_t n_kv, int64_t d, int64_t n_q, int64_t batch,
+                             const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
+                             const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
+                             float* partials, int32_t* counters, float scale, int32_t variant, const void* k_new,
+                             const void* v_new, int32_t kv_dtype, uint8_t* int4_pool_w, void* stream) {
   if (n_kv <= 0 || n_q % n_kv) return fail(KVMIX_EINVAL, "n_heads not a multiple of the pool's n_kv_heads");
   const int64_t gq = n_q / n_kv;
   if (gq > 8) return fail(KVMIX_EINVAL, "GQA group > 8 not supported");
@@ -1244,6 +1280,14 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
   a.part = partials;
   a.counters = counters;
   a.qscale = scale * LOG2E;
+  a.app_k = k_new;
+  a.app_v = v_new;
+  a.app_dtype = kv_dtype;
+  a.int4_pool_w = int4_pool_w;
+  if (k_new != nullptr) {
+    if (variant != 0) return fail(KVMIX_EINVAL, "the fused decode append runs in the tensor-core kernel (variant 0)");
+    if (!v_new || !int4_pool_w || kv_dtype < 0 || kv_dtype > 2) return fail(KVMIX_EINVAL, "bad append arguments");
+  }
   cudaStream_t s = (cudaStream_t)stream;
   switch (d) {
     case 32: return launch_decode<32>(a, n_cta, variant, s);
@@ -1251,4 +1295,30 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
     case 128: return launch_decode<128>(a, n_cta, variant, s);
     default: return fail(KVMIX_EINVAL, "decode supports head_dim 32, 64, 128");
   }
+}
+
+extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
+                                  const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
+                                  int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
+                                  int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
+                                  const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
+                                  const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
+                                  float scale, int32_t variant, void* stream) {
+  return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
+                           batch, page_indptr, page_ids, int4_indptr, int4_ids, work, cta_ptr, n_cta, partials,
+                           counters, scale, variant, nullptr, nullptr, 0, nullptr, stream);
+}
+
+extern "C" int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
+                                         uint8_t* int2_pool, uint8_t* int4_pool, int64_t pool_pages,
+                                         int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
+                                         int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
+                                         const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
+                                         const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
+                                         float scale, const void* k_new, const void* v_new, int32_t kv_dtype,
+                                         void* stream) {
+  if (!k_new || !v_new) return fail(KVMIX_EINVAL, "k_new / v_new are required");
+  return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
+                           batch, page_indptr, page_ids, int4_indptr, int4_ids, work, cta_ptr, n_cta, partials,
+                           counters, scale, 0, k_new, v_new, kv_dtype, int4_pool, stream);
 }

@@ -361,6 +361,27 @@ class MixedPrecisionPool:
         table._set_slots(np.append(table.slots, slot))
         return SlotAddress(slot)
 
+    def reserve_decode_slots(self, request_ids) -> np.ndarray:
+        """Slot bookkeeping of append_decode_token (pool.py:284-306), batched: pop one INT4
+        slot per request (LIFO, in request order) and append it to the request's partitioned
+        table.  The data is written later -- by append_decode_tokens, or by the fused
+        decode append of flash_decode_batched(..., append=...) one layer at a time."""
+        B = len(request_ids)
+        if len(self._free_int4) < B:
+            raise CapacityError("INT4 region exhausted during decode", region="int4")
+        for rid in request_ids:
+            t = self._tables.get(rid)
+            if t is None or not t.partitioned:
+                raise ValidationError(f"request {rid!r} unknown or not partitioned")
+        slots = np.empty(B, dtype=np.int64)
+        for i, rid in enumerate(request_ids):
+            s = self._free_int4.pop()
+            slots[i] = s
+            self._owner[s] = self._rid_index[rid]
+            t = self._tables[rid]
+            t._set_slots(np.append(t.slots, s))
+        return slots
+
     def append_decode_tokens(self, request_ids, k: torch.Tensor, v: torch.Tensor, layer: int | None = None,
                              slots: np.ndarray | None = None) -> np.ndarray:
         """Batched decode append (one token per request): k/v [B, L, Hkv, d], or
@@ -369,19 +390,7 @@ class MixedPrecisionPool:
         cfg = self.config
         B = len(request_ids)
         if slots is None:
-            if len(self._free_int4) < B:
-                raise CapacityError("INT4 region exhausted during decode", region="int4")
-            for rid in request_ids:
-                t = self._tables.get(rid)
-                if t is None or not t.partitioned:
-                    raise ValidationError(f"request {rid!r} unknown or not partitioned")
-            slots = np.empty(B, dtype=np.int64)
-            for i, rid in enumerate(request_ids):
-                s = self._free_int4.pop()
-                slots[i] = s
-                self._owner[s] = self._rid_index[rid]
-                t = self._tables[rid]
-                t._set_slots(np.append(t.slots, s))
+            slots = self.reserve_decode_slots(request_ids)
         ids = torch.as_tensor((slots - cfg.offset).astype(np.int32), device=self.device)
         if layer is None:
             lin, l0 = cfg.n_layers, 0

@@ -210,6 +210,56 @@ def test_decode_after_append(cuda):
         assert ok, err
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_fused_decode_append(cuda, dtype):
+    """K4 fused into K2: reserve one INT4 slot per request, then per layer one launch both
+    writes the new token (bit-exact with the reference INT4 TokenBlocks) and attends to it."""
+    L, H, Hq, d = 3, 2, 8, 128
+    rng = np.random.default_rng(9)
+    cfg = kv.PoolConfig(total_slots=8192, offset=4096, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(8192, 4096, L, H, d))
+    rids = [f"r{i}" for i in range(4)]
+    for i, rid in enumerate(rids):
+        n = int(rng.integers(30, 1500))
+        bits = np.where(rng.random(n) < 0.8, 2, 4)
+        k, v = rand_kv(70 + i, L, n, H, d)
+        t = pool.alloc(rid, bits)
+        op.alloc(rid, bits)
+        pool.write_prefill(t, k, v)
+        op.write_prefill(rid, k, v)
+        pool.partition(t)
+        op.partition(rid)
+    for step in range(3):
+        slots = pool.reserve_decode_slots(rids)
+        assert slots.tolist() == [op.pop_decode_slot(r) for r in rids]
+        b = kv.DecodeBatch(pool, rids, n_q_heads=Hq)
+        kn = torch.as_tensor(rng.standard_normal((len(rids), L, H, d)).astype(np.float32), device=cuda).to(dtype)
+        vn = torch.as_tensor(rng.standard_normal((len(rids), L, H, d)).astype(np.float32), device=cuda).to(dtype)
+        for i, rid in enumerate(rids):
+            op.write_decode(int(slots[i]), kn[i].float().cpu().numpy(), vn[i].float().cpu().numpy())
+        q = rng.standard_normal((L, len(rids), Hq, d)).astype(np.float32)
+        for layer in range(L):
+            out = kv.flash_decode_batched(torch.as_tensor(q[layer], device=cuda), b, layer,
+                                          append=(kn[:, layer], vn[:, layer])).cpu().numpy()
+            for i, rid in enumerate(rids):
+                ok, err = close(out[i], oatt.flash_decode_pool(q[layer, i], op, rid, layer))
+                assert ok, (step, layer, rid, err)
+    torch.cuda.synchronize()
+    assert_same_pool(pool, op)
+
+
+def assert_same_pool(pool, op):
+    from paper_2605_17170_b200 import layout
+    d, L, H = pool.config.head_dim, pool.config.n_layers, pool.config.n_kv_heads
+    i2 = pool.int2_pool[: L * H * pool.n_pages * pool.page_stride].view(L, H, pool.n_pages, pool.page_stride)
+    i4 = pool.int4_pool[: L * H * pool.n_int4 * pool.slot_stride].view(L, H, pool.n_int4, pool.slot_stride)
+    i2, i4 = i2.cpu().numpy(), i4.cpu().numpy()
+    assert np.array_equal(layout.page_payloads(i2[op.page_written], d), op.int2[op.page_written])
+    assert np.array_equal(i4[op.slot_written], layout.slot_records(op.int4[op.slot_written], d))
+    assert np.array_equal(pool._int4_written, op.slot_written)
+
+
 def test_cuda_graph_capture(cuda):
     pool, t, op, *_ = build(8, 3000, 2, 128, 0.8)
     batch = kv.DecodeBatch(pool, ["req"], n_q_heads=16)
