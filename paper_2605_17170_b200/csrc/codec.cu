@@ -331,22 +331,38 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
   extern __shared__ __align__(16) uint8_t psm[];
   uint8_t* srec = psm + 4 * P::TILE;
   const int tid = threadIdx.x;
-  auto fetch = [&](int64_t item, int stg) {  // issue the item's 2 x 32 rows into stage stg
-    const int64_t p = item % n_pages, lh = item / n_pages;
-    const int64_t l = lh / n_kv_heads, h = lh % n_kv_heads;
-    uint8_t* Ks = psm + 2 * stg * P::TILE;
-    for (int i = tid; i < 2 * G * P::CHUNKS; i += 128) {
-      const int tile = i / (G * P::CHUNKS), r = (i / P::CHUNKS) % G, ch = i % P::CHUNKS;
+  // Row source addresses of an item, computed once per row (64 threads) into a 2-stage
+  // table, then every 16 B chunk copy is one table read + one cp.async.
+  __shared__ const uint8_t* rowp[2][2 * G];
+  auto rows = [&](int64_t item, int stg) {
+    if (tid < 2 * G) {
+      const int64_t p = item % n_pages, lh = item / n_pages;
+      const int64_t l = lh / n_kv_heads, h = lh % n_kv_heads;
+      const int tile = tid / G, r = tid % G;
       const int t = page_tokens[p * G + r];
-      const T* src = (tile ? values : keys) + ((l * n_tokens + t) * n_kv_heads + h) * D;
-      cp_async16(staged<D, T>(Ks + tile * P::TILE, r, 16 * ch), reinterpret_cast<const uint4*>(src) + ch);
+      rowp[stg][tid] = reinterpret_cast<const uint8_t*>((tile ? values : keys) + ((l * n_tokens + t) * n_kv_heads + h) * D);
+    }
+  };
+  auto fetch = [&](int stg) {  // issue the item's 2 x 32 rows (table rowp[stg]) into stage stg
+    uint8_t* Ks = psm + 2 * stg * P::TILE;
+#pragma unroll 4
+    for (int i = tid; i < 2 * G * P::CHUNKS; i += 128) {
+      const int tr = i / P::CHUNKS, ch = i % P::CHUNKS;  // tr = tile * 32 + row
+      cp_async16(staged<D, T>(Ks + (tr / G) * P::TILE, tr % G, 16 * ch), rowp[stg][tr] + 16 * ch);
     }
   };
   int stg = 0;
-  if (blockIdx.x < n_items) fetch(blockIdx.x, 0);
+  if (blockIdx.x < n_items) {
+    rows(blockIdx.x, 0);
+    __syncthreads();
+    fetch(0);
+  }
   cp_async_commit();
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, stg ^= 1) {
-    if (item + gridDim.x < n_items) fetch(item + gridDim.x, stg ^ 1);
+    const bool more = item + gridDim.x < n_items;
+    if (more) rows(item + gridDim.x, stg ^ 1);
+    __syncthreads();
+    if (more) fetch(stg ^ 1);
     cp_async_commit();
     cp_async_wait<1>();  // this item's tiles have landed (the next item's may still fly)
     __syncthreads();
