@@ -751,8 +751,13 @@ __device__ __forceinline__ void prime_piece(const DecodeArgs& a, const Unit& u, 
   }
 }
 
+#ifdef KVMIX_MAXREG
+#define KVMIX_FUSED_BOUNDS __maxnreg__(KVMIX_MAXREG)
+#else
+#define KVMIX_FUSED_BOUNDS __launch_bounds__(NW * 32, KVMIX_MINB)
+#endif
 template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false, bool APPEND = false>
-__global__ void __launch_bounds__(NW * 32, KVMIX_MINB) decode_mma_kernel(const DecodeArgs a) {
+__global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[NW][STAGES];
