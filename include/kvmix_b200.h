@@ -118,7 +118,7 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
  *   ceil(n_int4/32) INT4 tiles of 32 slots, so every tile is bitwidth-homogeneous.
  *   work [n_pieces][8] = {unit, tile_lo, tile_hi, slot, part0, nparts, 0, 0}: a piece is a
  *     contiguous tile range of one unit; slot = -1 if the piece is the whole unit, else its
- *     partial slot in partials [n_parts][8][d + 2], the unit's partials being slots
+ *     partial slot in partials [n_parts][8][d + 4], the unit's partials being slots
  *     part0 .. part0 + nparts - 1.
  *   cta_ptr [n_cta + 1]: CTA i runs pieces cta_ptr[i] .. cta_ptr[i+1] (a byte-balanced share
  *     of the batch, see plan.py); the last CTA to finish a split unit merges its partials.

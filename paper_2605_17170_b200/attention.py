@@ -102,7 +102,7 @@ class DecodeBatch:
         self.n_cta = int(cta_ptr.size - 1)
         self.n_pieces = int(work.shape[0])
         self.n_parts = n_parts
-        self.partials = torch.empty(max(1, n_parts) * 8 * (cfg.head_dim + 2), dtype=torch.float32, device=dev)
+        self.partials = torch.empty(max(1, n_parts) * 8 * (cfg.head_dim + 4), dtype=torch.float32, device=dev)
         self.counters = torch.zeros(self.batch * cfg.n_kv_heads, dtype=torch.int32, device=dev)
         self.n_tokens = t["n_pages"] * cfg.page_size + t["n_int4"]
         # newest INT4 slot of each request (the fused decode append's target), host side

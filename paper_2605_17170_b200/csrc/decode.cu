@@ -45,7 +45,10 @@ namespace kvmix {
 #define KVMIX_BATCHIDS 0  // 1: INT2 page ids 32 tiles per coalesced load (measured neutral)
 #endif
 constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
-constexpr int NW = 4;                 // warps per CTA
+#ifndef KVMIX_NW
+#define KVMIX_NW 4
+#endif
+constexpr int NW = KVMIX_NW;          // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_SLACK = 8.f;  // see softmax_tile
@@ -80,7 +83,7 @@ struct DecodeArgs {
   const int32_t* int4_ids;
   const int32_t* work;     // pieces [n][8]: unit, tile_lo, tile_hi, slot (-1: whole unit), part0, nparts
   const int32_t* cta_ptr;  // [grid + 1]: pieces of CTA i are cta_ptr[i] .. cta_ptr[i+1]
-  float* part;             // split partials [n_parts][8][D + 2] (acc[D], m, l; log2 domain)
+  float* part;             // split partials [n_parts][8][D + 4] (acc[D], m, l, pad; log2 domain)
   int32_t* counters;       // [batch * n_kv] arrival counters, zero between launches
   float qscale;            // softmax scale * log2(e)
   // K4 fused decode append (variant 0): each request's newest token -- the last INT4 entry of
@@ -156,7 +159,7 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
     if (u.slot < 0) {
       store_out(a, obase + i, acc / l);
     } else {
-      float* pp = a.part + ((int64_t)u.slot * 8 + hh) * (D + 2);
+      float* pp = a.part + ((int64_t)u.slot * 8 + hh) * (D + 4);
       pp[c] = acc;
       if (c == 0) {
         pp[D] = M;
@@ -176,20 +179,48 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
   __syncthreads();
   if (!*sm_flag) return;
   __threadfence();
-  for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
-    const int hh = i / D, c = i % D;
-    const float* p0 = a.part + ((int64_t)u.part0 * 8 + hh) * (D + 2);
-    constexpr int64_t PSTR = 8 * (D + 2);
-    float M = -INFINITY;
-    for (int k = 0; k < u.nparts; ++k) M = fmaxf(M, __ldcg(p0 + k * PSTR + D));
-    float acc = 0.f, l = 0.f;
-    for (int k = 0; k < u.nparts; ++k) {
-      const float mk = __ldcg(p0 + k * PSTR + D);
-      const float f = mk == -INFINITY ? 0.f : fast_exp2(mk - M);
-      acc = fmaf(__ldcg(p0 + k * PSTR + c), f, acc);
-      l = fmaf(__ldcg(p0 + k * PSTR + D + 1), f, l);
+  // The last CTA merges the unit's partials: a thread owns 4 channels of one head and pulls
+  // the partials 8 at a time with all loads in flight together (one L2 round trip per 8
+  // partials, not three per partial), merging online.
+  constexpr int64_t PSTR = 8 * (D + 4);
+  for (int i = threadIdx.x; i < a.gq * D / 4; i += blockDim.x) {
+    const int hh = (4 * i) / D, c0 = (4 * i) % D;
+    const float* p0 = a.part + ((int64_t)u.part0 * 8 + hh) * (D + 4);
+    float M = -INFINITY, l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k0 = 0; k0 < u.nparts; k0 += 8) {
+      float mk[8], lk[8];
+      float4 ak[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = k0 + e < u.nparts;
+        const float* pk = p0 + (int64_t)(ok ? k0 + e : k0) * PSTR;
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(pk + D));
+        mk[e] = ok ? ml.x : -INFINITY;
+        lk[e] = ml.y;
+        ak[e] = __ldcg(reinterpret_cast<const float4*>(pk + c0));
+      }
+      float Mn = M;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) Mn = fmaxf(Mn, mk[e]);
+      const float f = M == -INFINITY ? 0.f : fast_exp2(M - Mn);
+      acc.x *= f; acc.y *= f; acc.z *= f; acc.w *= f;
+      l *= f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float g = mk[e] == -INFINITY ? 0.f : fast_exp2(mk[e] - Mn);
+        acc.x = fmaf(ak[e].x, g, acc.x); acc.y = fmaf(ak[e].y, g, acc.y);
+        acc.z = fmaf(ak[e].z, g, acc.z); acc.w = fmaf(ak[e].w, g, acc.w);
+        l = fmaf(lk[e], g, l);
+      }
+      M = Mn;
     }
-    store_out(a, obase + i, acc / l);
+    const float inv = 1.f / l;
+    const int64_t oi = obase + (int64_t)hh * D + c0;
+    store_out(a, oi, acc.x * inv);
+    store_out(a, oi + 1, acc.y * inv);
+    store_out(a, oi + 2, acc.z * inv);
+    store_out(a, oi + 3, acc.w * inv);
   }
 }
 
@@ -772,8 +803,10 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
     fence_mbar_init();
   }
   __syncwarp();
+  pdl_launch_dependents();  // the next kernel may start prefetching its KV tiles
   int stage = 0;  // ring position and mbarrier phase persist across pieces
   uint32_t phase = 0;
+  bool waited = false;  // q, out, partials and counters are touched only after pdl_wait()
 
   const int piece_end = a.cta_ptr[blockIdx.x + 1];
   bool primed = false;  // the piece's first tiles were issued while the previous piece merged
@@ -819,6 +852,12 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   int meta_next = load_meta(STAGES), meta_next2 = load_meta(STAGES + 1);  // metas run two tiles ahead
 
   // ---- Q fragments (see QFrag): built once per CTA by warp 0 into shared memory ----
+  // The KV tiles above are this launch's own inputs (written by earlier steps); q, out and
+  // the split scratch may belong to the previous kernel in the stream, so wait for it here.
+  if (!waited) {
+    pdl_wait();
+    waited = true;
+  }
   uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + NW * STAGES * C::BUF);
   if (warp == 0) build_qtab<D, LO>(a, u, qtab, lane);
   __syncthreads();
@@ -1000,6 +1039,7 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_wait();
   uint32_t kg = 0;  // tiles this pair has run so far (both warps count identically)
 
   for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
@@ -1114,6 +1154,7 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
   __shared__ float sm_m[NW * 8], sm_l[NW * 8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   __shared__ int sm_flag;
+  pdl_wait();
   for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
   const Unit u = load_unit(a, piece);
   for (int i = threadIdx.x; i < 8 * D; i += blockDim.x) {
@@ -1197,7 +1238,20 @@ static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_cta, int smem
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
   }
-  kern<<<(unsigned)n_cta, nwarps * 32, smem, s>>>(a);
+  // programmatic dependent launch: this grid may start while the previous kernel in the
+  // stream drains; the kernel waits (griddepcontrol.wait) before touching q / out / scratch
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n_cta);
+  cfg.blockDim = dim3(nwarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
   return check_launch("flash_decode");
 }
 
