@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--int2-frac", type=float, default=None, help="override: i.i.d. bits with this INT2 fraction")
     ap.add_argument("--ctas-per-sm", type=int, default=3, help="stream-K planner: resident CTAs per SM")
-    ap.add_argument("--int4-weight", type=float, default=1.0, help="stream-K planner: cost weight of INT4 bytes")
+    ap.add_argument("--int4-weight", type=float, default=0.9, help="stream-K planner: cost weight of INT4 bytes")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the K1 quantize+pack (cfg3 slice) measurement")

@@ -247,13 +247,16 @@ def test_plan_covers_every_tile_once(B, Hkv, n_cta):
     assert sorted(slots) == list(range(n_parts))
 
 
-def test_plan_byte_balance():
+@pytest.mark.parametrize("w4", [1.0, 0.9])
+def test_plan_cost_balance(w4):
+    """Every CTA gets the same cost: bytes, with INT4 bytes weighted by int4_weight."""
     npg, n4 = np.array([1000] * 16), np.array([6000] * 16)
-    work, cta_ptr, _ = plan_stream(npg, n4, 8, 3072, 160, n_cta=444)
+    work, cta_ptr, _ = plan_stream(npg, n4, 8, 3072, 160, n_cta=444, int4_weight=w4)
+    cost = np.array([b if i < 1000 else b * w4 for i, b in enumerate(_tile_bytes(1000, 6000))])
     per_cta = np.zeros(444)
     for c in range(444):
         for u, lo, hi in work[cta_ptr[c]:cta_ptr[c + 1], :3]:
-            per_cta[c] += sum(_tile_bytes(1000, 6000)[lo:hi])
+            per_cta[c] += cost[lo:hi].sum()
     assert per_cta.max() / per_cta.mean() < 1.02 and per_cta.min() / per_cta.mean() > 0.98
 
 
