@@ -63,9 +63,13 @@ struct Cfg {
   static constexpr int PS = page_stride(D);
   static constexpr int SS = slot_stride(D);
   static constexpr int BUF = PS > 32 * SS ? PS : 32 * SS;  // one INT2 page or 32 INT4 slots (slot-contiguous)
-  static constexpr int QTAB = (D / 8 + 2) * 32 * 8 * 2;         // q fragment table (LO size)
+  static constexpr int QTAB = (4 * NCH + 2) * 32 * 8;             // q fragment table (LO size)
   static constexpr int MERGE = (NW * 8 * D + 2 * NW * 8) * 4;     // per-warp (acc, m, l) for the piece merge
-  static constexpr int SMEM = NW * STAGES * BUF + QTAB + MERGE;
+  // MERGE_IN_RING: the piece merge reuses the (idle) ring, so 4 CTAs fit per SM; the next
+  // piece's first copies then start after the merge instead of during it.
+  static constexpr bool MERGE_IN_RING = KVMIX_MINB >= 4;
+  static_assert(!MERGE_IN_RING || MERGE <= NW * STAGES * BUF, "merge scratch must fit in the ring");
+  static constexpr int SMEM = NW * STAGES * BUF + QTAB + (MERGE_IN_RING ? 0 : MERGE);
 };
 
 struct DecodeArgs {
@@ -842,6 +846,7 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
     issue_tile<D>(u, u.tlo + warp + k * NW, meta, ring + s * C::BUF, &bars[warp][s], lane, kv2, kv4);
   };
   if (MEMORY && !primed) {
+    if (C::MERGE_IN_RING) fence_proxy_async();  // the previous piece merged through the ring
     int s0 = stage;  // the ring continues where the previous piece left it
     for (int k = 0; k < STAGES && k < nmine; ++k) {
       issue(k, load_meta(k), s0);
@@ -967,7 +972,7 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
 #endif
 
   // ---- the next piece's first tiles stream in while this one merges (the ring is idle) ----
-  if (MEMORY && piece + 1 < piece_end) {
+  if (MEMORY && !C::MERGE_IN_RING && piece + 1 < piece_end) {
     prime_piece<D>(a, load_unit(a, piece + 1), warp, lane, ring, bars, stage);
     primed = true;
   }
@@ -975,7 +980,7 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   const float l0 = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[0], 28 + q);  // row 7 >= NG
   const float l1 = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[1], 28 + q);
   __syncthreads();  // every warp is done with the q table and the previous merge scratch
-  float* sm_acc = reinterpret_cast<float*>(smem + NW * STAGES * C::BUF + C::QTAB);
+  float* sm_acc = reinterpret_cast<float*>(C::MERGE_IN_RING ? smem : smem + NW * STAGES * C::BUF + C::QTAB);
   float* sm_m = sm_acc + NW * 8 * D;
   float* sm_l = sm_m + NW * 8;
   store_warp_acc<D>(acc, sm_acc, warp, lane);
