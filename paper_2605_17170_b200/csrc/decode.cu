@@ -45,6 +45,9 @@ namespace kvmix {
 #define KVMIX_BATCHIDS 0  // 1: INT2 page ids 32 tiles per coalesced load (measured neutral)
 #endif
 constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
+#ifndef KVMIX_LAZYPARAM
+#define KVMIX_LAZYPARAM 0  // 1: INT2 key scale/zero quads loaded per chunk pair (fewer live registers)
+#endif
 #ifndef KVMIX_NW
 #define KVMIX_NW 4
 #endif
@@ -422,17 +425,22 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
   using C = Cfg<D>;
   constexpr int KB = D / 4, LB = KB < 16 ? KB : 16;
   const int g = lane >> 2, q = lane & 3;
-  uint32_t kw[C::NCH], ksw[2 * C::NCH], kzw[2 * C::NCH];
+  uint32_t kw[C::NCH];
 #pragma unroll
   for (int o = 0; o < KB; o += LB) {
     const int p = q * KB + o;
     lds_vec<LB>(buf + g * D + ((((p >> 4) ^ (g & 1)) << 4) | (p & 15)), kw + o / 4);
   }
+#if KVMIX_LAZYPARAM
+  uint32_t ksw[4], kzw[4];  // the quad of the current chunk pair only (lower register pressure)
+#else
+  uint32_t ksw[2 * C::NCH], kzw[2 * C::NCH];
 #pragma unroll
   for (int i = 0; i < KB / 8; ++i) {  // 16 B chunk i of lane q at chunk 4i + q
     lds_vec<16>(buf + PG_KS(D) + (4 * i + q) * 16, ksw + 4 * i);
     lds_vec<16>(buf + PG_KZ(D) + (4 * i + q) * 16, kzw + 4 * i);
   }
+#endif
   // two accumulators per M tile (even / odd chunks) halve the HMMA dependency chains
   float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, d0[4] = {0.f, 0.f, 0.f, 0.f},
         d1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -441,7 +449,15 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
   float cbE[4] = {0.f, 0.f, 0.f, 0.f}, cbO[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < C::NCH; ++i) {
+#if KVMIX_LAZYPARAM
+    const int P4 = 0, odd = i & 1;
+    if (!odd) {
+      lds_vec<16>(buf + PG_KS(D) + (4 * (i >> 1) + q) * 16, ksw);
+      lds_vec<16>(buf + PG_KZ(D) + (4 * (i >> 1) + q) * 16, kzw);
+    }
+#else
     const int P4 = 4 * (i >> 1), odd = i & 1;
+#endif
     const uint32_t w = kw[i], x = w >> 8;
     const uint64_t qi = qf.b2(i);
     const uint64_t qs = pack_b64(hmul2u(lo32(qi), ksw[P4 + odd]), hmul2u(hi32(qi), ksw[P4 + 2 + odd]));
