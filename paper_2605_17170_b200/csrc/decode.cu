@@ -45,6 +45,9 @@ namespace kvmix {
 #define KVMIX_BATCHIDS 0  // 1: INT2 page ids 32 tiles per coalesced load (measured neutral)
 #endif
 constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
+#ifndef KVMIX_TILEFENCE
+#define KVMIX_TILEFENCE 0  // 1: proxy fence before every tile copy (not needed without the fused append)
+#endif
 #ifndef KVMIX_LAZYPARAM
 #define KVMIX_LAZYPARAM 0  // 1: INT2 key scale/zero quads loaded per chunk pair (fewer live registers)
 #endif
@@ -977,7 +980,11 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
     }
     __syncwarp();
     if (MEMORY && k + STAGES < nmine) {
-      fence_proxy_async();
+      // Reads-before-async-writes: every lane's LDS of this slot has completed (its values were
+      // consumed above, before __syncwarp), so the copy may overwrite the slot without a proxy
+      // fence -- the same release a TMA consumer gives its producer through an mbarrier.  The
+      // fused append wrote the slot through the generic proxy, so that path keeps the fence.
+      if (APPEND || KVMIX_TILEFENCE) fence_proxy_async();
       issue(k + STAGES, meta, stage);
     }
     if (++stage == STAGES) {
