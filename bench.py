@@ -344,6 +344,7 @@ def measure_k1(args, device, peak) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
+    route = measure_route(bits, cfg, device)
     bytes_in = 2 * k.numel() * k.element_size()
     bytes_out = L * H * (n_pages * pool.page_stride + n4 * 2 * kv.token_block_payload_bytes(d, 4))
     gbs = (bytes_in + bytes_out) / (ms / 1000.0) / 1e9
@@ -352,7 +353,65 @@ def measure_k1(args, device, peak) -> dict:
     return {"workload": "cfg3 slice: 128K-token tagged trace, 8 of 64 layers, 8 kv heads, d=128, bf16 in",
             "ms_per_call": ms, "ms_per_layer": ms / L, "cfg3_ms_64_layers": ms / L * 64,
             "bytes_in": bytes_in, "bytes_out": int(bytes_out), "achieved_gbs": gbs, "frac": gbs / peak,
-            "stored_int2_fraction": n_pages * g / N, "kernels": "prefill_pages_kernel + int4_tokens_kernel"}
+            "stored_int2_fraction": n_pages * g / N, "kernels": "prefill_pages_kernel + int4_tokens_kernel",
+            "k6_route": route}
+
+
+def measure_route(bits, cfg, device) -> dict:
+    """K6 (device-side page-table build) on the same 128K-token request: the two routing
+    kernels alone (CUDA events), alloc_device end to end (wall, incl. the count read-back,
+    pops and the slots download) and the host allocator (wall) for comparison."""
+    import time
+
+    import torch
+
+    import paper_2605_17170_b200 as kv
+    from paper_2605_17170_b200 import _lib
+    g, n = cfg.page_size, bits.size
+    bd = torch.as_tensor(bits, device=device).to(torch.int8)
+    n_pages = int((bits == 2).sum()) // g
+    m = n - n_pages * g
+    st = torch.arange(n_pages, device=device, dtype=torch.int64) * g
+    po = torch.arange(m, device=device, dtype=torch.int64) + cfg.offset
+    slots = torch.empty(n, dtype=torch.int64, device=device)
+    pt = torch.empty(n_pages * g, dtype=torch.int32, device=device)
+    pi = torch.empty(n_pages, dtype=torch.int32, device=device)
+    it = torch.empty(m, dtype=torch.int32, device=device)
+    ii = torch.empty(m, dtype=torch.int32, device=device)
+    err = torch.zeros(1, dtype=torch.int32, device=device)
+    cnt = torch.zeros(int(_lib.lib.kvmix_route_scratch_elems(n)), dtype=torch.int64, device=device)
+
+    def kernels():
+        _lib.check(_lib.lib.kvmix_count_int2(bd.data_ptr(), n, cnt.data_ptr(), err.data_ptr(), _lib.stream()))
+        _lib.check(_lib.lib.kvmix_route_tokens(bd.data_ptr(), n, g, cnt.data_ptr(), st.data_ptr(), n_pages,
+                                               po.data_ptr(), m,
+                                               cfg.offset, slots.data_ptr(), pt.data_ptr(), pi.data_ptr(),
+                                               it.data_ptr(), ii.data_ptr(), err.data_ptr(), _lib.stream()))
+    kernels()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        kernels()
+    e1.record()
+    torch.cuda.synchronize()
+    kern_ms = e0.elapsed_time(e1) / 10
+
+    def wall(fn, reps=5):
+        best = float("inf")
+        for r in range(reps):
+            pool = kv.MixedPrecisionPool(cfg, device=device)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn(pool, f"r{r}")
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+            del pool
+        return best * 1e3
+    dev_ms = wall(lambda p, rid: p.alloc_device(rid, bd))
+    host_ms = wall(lambda p, rid: p.alloc(rid, bits))
+    return {"tokens": int(n), "kernels_ms": kern_ms, "alloc_device_ms": dev_ms, "alloc_host_ms": host_ms,
+            "kernels": "count_int2_kernel + route_tokens_kernel"}
 
 
 def run_ours(args):

@@ -106,6 +106,31 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
                          int64_t offset, int64_t layer, int64_t n_kv_heads, int64_t head_dim, const int32_t* slots,
                          int64_t m, float* k_out, float* v_out, void* stream);
 
+/* ---- device-side page-table build (K6) ----------------------------------------------- */
+
+/* Scratch size (int64 elements) of the routing counts for an n-token request. */
+int64_t kvmix_route_scratch_elems(int64_t n);
+
+/* Phase 1 of pool.py:122 alloc on the device: counts[0] = number of bitwidth-2 tokens of
+ * bits[n] (int8, device), counts[1..] = per-chunk counts used by kvmix_route_tokens
+ * (counts: device int64 [kvmix_route_scratch_elems(n)]).  Bits other than 2 / 4 set err bit 2.
+ * The host reads counts[0] to pop its LIFO stacks (pool.py:131-148). */
+int kvmix_count_int2(const int8_t* bits, int64_t n, int64_t* counts, int32_t* err_flag, void* stream);
+
+/* Phase 2: replaces the O(N) token routing of pool.py:122-163 alloc and the index emission of
+ * pool.py:228-262 write_prefill.  The host pops n_pages = counts[0] / page_size page starts and
+ * n_int4 = n - n_pages * page_size INT4 slots (pop order) and passes them with the counts of
+ * phase 1; the kernel writes
+ *   slots[n]                       the PageTable (token order), identical to the host alloc
+ *   page_tokens[n_pages][page_size], page_ids[n_pages]   K1 page inputs   (nullable)
+ *   int4_tokens[n_int4], int4_ids[n_int4] (slot - offset) K1 INT4 inputs / K2 INT4 list (nullable)
+ * The r-th INT2 token with r < n_pages * page_size gets page_starts[r / page_size] + r % page_size;
+ * every other token takes the next INT4 pop in token order. */
+int kvmix_route_tokens(const int8_t* bits, int64_t n, int32_t page_size, const int64_t* counts,
+                       const int64_t* page_starts, int64_t n_pages, const int64_t* int4_pops, int64_t n_int4,
+                       int64_t offset, int64_t* slots, int32_t* page_tokens, int32_t* page_ids,
+                       int32_t* int4_tokens, int32_t* int4_ids, int32_t* err_flag, void* stream);
+
 /* ---- decode attention (K2 + K3) ---------------------------------------------------- */
 
 /* Replaces attention.py:175 flash_decode (+ PoolView.gather pool.py:394, _split_partial

@@ -54,6 +54,10 @@ _SIGS = {
     "kvmix_flash_decode_append": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P,
                                    _P, _P, _P, _I64, _P, _P, _F, _P, _P, _I32, _P], ctypes.c_int),
     "kvmix_merge_partials": ([_P, _P, _P, _I64, _I64, _P, _P], ctypes.c_int),
+    "kvmix_route_scratch_elems": ([_I64], _I64),
+    "kvmix_count_int2": ([_P, _I64, _P, _P, _P], ctypes.c_int),
+    "kvmix_route_tokens": ([_P, _I64, _I32, _P, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P],
+                           ctypes.c_int),
 }
 
 for _name, (_args, _ret) in _SIGS.items():

@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from ._lib import lib
-from .errors import CapacityError, ValidationError
+from .errors import CapacityError, KvmixError, ValidationError
 from .quant import GROUP_SIZE, key_page_payload_bytes, token_block_payload_bytes
 
 SUPPORTED_HEAD_DIMS = (32, 64, 128, 256)
@@ -46,6 +46,9 @@ class PageTable:
         self.slots = np.asarray(slots if slots is not None else [], dtype=np.int64)
         self.partitioned = partitioned
         self._entries_cache = None
+        # (page_tokens, page_ids, int4_tokens, int4_ids) device tensors left by alloc_device
+        # (K6) for write_prefill; dropped whenever the slots change
+        self._dev_index = None
 
     @property
     def entries(self) -> list[SlotAddress]:
@@ -61,6 +64,7 @@ class PageTable:
     def _set_slots(self, slots) -> None:
         self.slots = np.asarray(slots, dtype=np.int64)
         self._entries_cache = None
+        self._dev_index = None
 
     def __len__(self) -> int:
         return int(self.slots.size)
@@ -185,6 +189,65 @@ class MixedPrecisionPool:
         self._tables[request_id] = table
         return table
 
+    def alloc_device(self, request_id: str, per_token_bitwidths) -> PageTable:
+        """alloc (pool.py:122-163) with the O(N) token routing on the GPU (K6): the bits are
+        counted on the device, the host pops its LIFO stacks exactly as alloc does, and
+        kvmix_route_tokens writes the table and the K1 index lists.  The resulting slots are
+        identical to alloc's; the index lists stay on the device for write_prefill."""
+        if request_id in self._tables:
+            raise ValidationError(f"request {request_id!r} already live")
+        dev = self.device
+        bits = torch.as_tensor(np.asarray(per_token_bitwidths) if not torch.is_tensor(per_token_bitwidths)
+                               else per_token_bitwidths, device=dev).reshape(-1)
+        if bits.dtype != torch.int8:  # values must survive the int8 narrowing (the kernel checks 2 / 4)
+            if not bool(((bits == 2) | (bits == 4)).all()):
+                raise ValidationError("per-token bitwidths must be 2 or 4")
+            bits = bits.to(torch.int8)
+        bits = bits.contiguous()
+        n = int(bits.numel())
+        g = self.config.page_size
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        counts = torch.empty(int(lib.kvmix_route_scratch_elems(n)), dtype=torch.int64, device=dev)
+        _lib.check(lib.kvmix_count_int2(bits.data_ptr(), n, counts.data_ptr(), err.data_ptr(), _lib.stream()))
+        n2 = int(counts[0].item())
+        if int(err.item()) & 2:
+            raise ValidationError("per-token bitwidths must be 2 or 4")
+        n_pages = n2 // g
+        m = n - n_pages * g
+        if n_pages > len(self._free_pages):
+            raise CapacityError(f"INT2 region exhausted: need {n_pages} pages, {len(self._free_pages)} free",
+                                region="int2")
+        if m > len(self._free_int4):
+            raise CapacityError(f"INT4 region exhausted: need {m} slots, {len(self._free_int4)} free", region="int4")
+        starts = np.asarray(self._free_pages[-n_pages:][::-1] if n_pages else [], dtype=np.int64)
+        pops = np.asarray(self._free_int4[-m:][::-1] if m else [], dtype=np.int64)
+        if n_pages:
+            del self._free_pages[-n_pages:]
+        if m:
+            del self._free_int4[-m:]
+        st = torch.as_tensor(starts, device=dev)
+        po = torch.as_tensor(pops, device=dev)
+        slots = torch.empty(n, dtype=torch.int64, device=dev)
+        pt = torch.empty((n_pages, g), dtype=torch.int32, device=dev)
+        pi = torch.empty(n_pages, dtype=torch.int32, device=dev)
+        it = torch.empty(m, dtype=torch.int32, device=dev)
+        ii = torch.empty(m, dtype=torch.int32, device=dev)
+        _lib.check(lib.kvmix_route_tokens(
+            bits.data_ptr(), n, g, counts.data_ptr(), st.data_ptr(), n_pages, po.data_ptr(), m, self.config.offset,
+            slots.data_ptr(), pt.data_ptr(), pi.data_ptr(), it.data_ptr(), ii.data_ptr(), err.data_ptr(),
+            _lib.stream()))
+        host = slots.cpu().numpy()
+        if int(err.item()):
+            raise KvmixError("device routing disagreed with the host counts")
+        rix = self._next_rid
+        self._next_rid += 1
+        self._rid_index[request_id] = rix
+        self._owner[host] = rix
+        table = PageTable(request_id=request_id, slots=host)
+        table._dev_index = (pt, pi, it, ii)
+        self._tables[request_id] = table
+        return table
+
     def free(self, request_id: str) -> None:
         """pool.py:165-188: INT4 slots pushed in entry order, pages in descending start order."""
         table = self._tables.pop(request_id, None)
@@ -285,20 +348,25 @@ class MixedPrecisionPool:
             v = v.to(k.dtype)
         s = table.slots
         is2 = s < cfg.offset
-        t2 = np.flatnonzero(is2)
-        t4 = np.flatnonzero(~is2)
-        if t2.size % g:
-            raise ValidationError("INT2 tokens of a table must fill whole pages")
-        page_tokens = t2.reshape(-1, g)
-        page_ids = s[page_tokens[:, 0]] // g if t2.size else np.zeros(0, np.int64)
-        dev = self.device
-        pt = torch.as_tensor(page_tokens.astype(np.int32), device=dev)
-        pi = torch.as_tensor(page_ids.astype(np.int32), device=dev)
-        it = torch.as_tensor(t4.astype(np.int32), device=dev)
-        ii = torch.as_tensor((s[t4] - cfg.offset).astype(np.int32), device=dev)
+        if table._dev_index is not None:  # index lists routed on the device (alloc_device)
+            pt, pi, it, ii = table._dev_index
+            page_ids = s[is2][::g] // g
+            t4 = np.flatnonzero(~is2)
+        else:
+            t2 = np.flatnonzero(is2)
+            t4 = np.flatnonzero(~is2)
+            if t2.size % g:
+                raise ValidationError("INT2 tokens of a table must fill whole pages")
+            page_tokens = t2.reshape(-1, g)
+            page_ids = s[page_tokens[:, 0]] // g if t2.size else np.zeros(0, np.int64)
+            dev = self.device
+            pt = torch.as_tensor(page_tokens.astype(np.int32), device=dev)
+            pi = torch.as_tensor(page_ids.astype(np.int32), device=dev)
+            it = torch.as_tensor(t4.astype(np.int32), device=dev)
+            ii = torch.as_tensor((s[t4] - cfg.offset).astype(np.int32), device=dev)
         _lib.check(lib.kvmix_write_prefill(
             k.data_ptr(), v.data_ptr(), _lib.dtype_code(k), cfg.n_layers, n, cfg.n_kv_heads, cfg.head_dim,
-            pt.data_ptr(), pi.data_ptr(), page_tokens.shape[0], it.data_ptr(), ii.data_ptr(), t4.size,
+            pt.data_ptr(), pi.data_ptr(), pi.numel(), it.data_ptr(), ii.data_ptr(), it.numel(),
             self.int2_pool.data_ptr(), self.n_pages, self.int4_pool.data_ptr(), self.n_int4,
             self._err.data_ptr(), _lib.stream()))
         if check_finite:

@@ -241,3 +241,57 @@ def test_fuzz_safety(cuda):
         except kv.CapacityError:
             pass
         pool.check_invariants()
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_alloc_device_matches_alloc_and_oracle(cuda, d):
+    """K6 (device-side routing, pool.py:122-163): the same slots as the host allocator and
+    the oracle, through frees that scramble the LIFO stacks, and the device index lists feed
+    write_prefill to the oracle's exact image."""
+    L, H = 2, 2
+    cfg = kv.PoolConfig(total_slots=120000, offset=60000, n_layers=L, n_kv_heads=H, head_dim=d)
+    dev_pool, host_pool = kv.MixedPrecisionPool(cfg), kv.MixedPrecisionPool(cfg)
+    op = opool.OraclePool(opool.Config(120000, 60000, L, H, d))
+    rng = np.random.default_rng(600 + d)
+    sizes = [0, 1, 31, 32, 33, 64, 700, 16384, 16385, 20000]
+    for r, n in enumerate(sizes):
+        p2 = [0.8, 1.0, 0.0, 0.5][r % 4]
+        bits = np.where(rng.random(n) < p2, 2, 4).astype(np.int64)
+        src = torch.as_tensor(bits, device=cuda).to(torch.int8) if r % 2 else bits
+        td = dev_pool.alloc_device(f"r{r}", src)
+        th = host_pool.alloc(f"r{r}", bits)
+        assert td.slots.tolist() == th.slots.tolist() == op.alloc(f"r{r}", bits)
+        if n and n <= 700:
+            k, v = rand_kv(r, L, n, H, d)
+            kt, vt = torch.as_tensor(k, device=cuda), torch.as_tensor(v, device=cuda)
+            dev_pool.write_prefill(td, kt, vt)
+            op.write_prefill(f"r{r}", k, v)
+        if r in (4, 7):  # free an earlier request: later pops come from a reordered stack
+            for p in (dev_pool, host_pool):
+                p.free(f"r{r - 2}")
+            op.free(f"r{r - 2}")
+    torch.cuda.synchronize()
+    assert_same_image(dev_pool, op)
+    dev_pool.check_invariants()
+    assert dev_pool.free_counts() == host_pool.free_counts()
+
+
+def test_alloc_device_errors(cuda):
+    cfg = kv.PoolConfig(total_slots=1024, offset=512, n_layers=1, n_kv_heads=1, head_dim=64)
+    pool = kv.MixedPrecisionPool(cfg)
+    with pytest.raises(kv.ValidationError):
+        pool.alloc_device("a", np.array([2, 3, 4]))
+    with pytest.raises(kv.ValidationError):
+        pool.alloc_device("a", torch.tensor([2, 4, 5], dtype=torch.int8, device=cuda))
+    with pytest.raises(kv.CapacityError):
+        pool.alloc_device("a", np.full(600, 2))
+    with pytest.raises(kv.CapacityError):
+        pool.alloc_device("a", np.full(600, 4))
+    before = pool.free_counts()
+    t = pool.alloc_device("a", np.full(64, 2))  # failed calls popped nothing
+    assert pool.free_counts() == (before[0] - 64, before[1])
+    with pytest.raises(kv.ValidationError):
+        pool.alloc_device("a", np.full(4, 2))
+    pool.free("a")
+    assert len(t) == 64
+    pool.check_invariants()
