@@ -60,6 +60,10 @@ _SIGS = {
                            ctypes.c_int),
 }
 
+if hasattr(lib, "kvmix_debug_cta_times"):  # debug builds (-DKVMIX_CTA_TIMES) only
+    lib.kvmix_debug_cta_times.argtypes = [_P, ctypes.c_int]
+    lib.kvmix_debug_cta_times.restype = ctypes.c_int
+
 for _name, (_args, _ret) in _SIGS.items():
     _fn = getattr(lib, _name)
     _fn.argtypes = _args

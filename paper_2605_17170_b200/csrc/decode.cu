@@ -75,7 +75,9 @@ struct Cfg {
   // piece's first copies then start after the merge instead of during it.
   static constexpr bool MERGE_IN_RING = KVMIX_MINB >= 4;
   static_assert(!MERGE_IN_RING || MERGE <= NW * STAGES * BUF, "merge scratch must fit in the ring");
-  static constexpr int SMEM = NW * STAGES * BUF + QTAB + (MERGE_IN_RING ? 0 : MERGE);
+  static constexpr int QS = D + 4;                                // raw q row stride (floats; 4-way LDS conflicts at most)
+  static constexpr int QRAW = 8 * QS * 4;                          // the unit's raw q [8 heads][D] (fp32) for build_qtab
+  static constexpr int SMEM = NW * STAGES * BUF + QTAB + (MERGE_IN_RING ? 0 : MERGE) + QRAW;
 };
 
 struct DecodeArgs {
@@ -724,15 +726,42 @@ __device__ __forceinline__ void store_warp_acc(const Acc<D>& acc, float* sm_acc,
   }
 }
 
-// Q fragments of one unit (see QFrag) written by one warp into the CTA's smem table.
+// The unit's q rows [gq][D] -> fp32 smem rows of stride QS (rows gq..7 zero), all threads,
+// every global load in flight at once (one L2 round trip instead of one per table entry).
+template <int D>
+__device__ __forceinline__ void stage_q(const DecodeArgs& a, const Unit& u, float* qraw) {
+  using C = Cfg<D>;
+  for (int i = 4 * (int)threadIdx.x; i < 8 * D; i += 4 * (int)blockDim.x) {
+    const int h = i / D, c = i % D;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (h < a.gq) {
+      const int64_t idx = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + h) * D + c;
+      if (a.q_dtype == KVMIX_F32) {
+        v = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.q) + idx);
+      } else {
+        const uint2 w = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.q) + idx);
+        if (a.q_dtype == KVMIX_BF16) {
+          v = make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u),
+                          __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u));
+        } else {
+          const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+          const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+          v = make_float4(lo.x, lo.y, hi.x, hi.y);
+        }
+      }
+    }
+    *reinterpret_cast<float4*>(qraw + h * C::QS + c) = v;
+  }
+}
+
+// Q fragments of one unit (see QFrag) written by one warp into the CTA's smem table, from
+// the unit's staged q rows (stage_q).
 template <int D, bool LO>
-__device__ __forceinline__ void build_qtab(const DecodeArgs& a, const Unit& u, uint64_t* qtab, int lane) {
+__device__ __forceinline__ void build_qtab(const float* qraw, uint64_t* qtab, int lane) {
   using C = Cfg<D>;
   using QF = QFrag<D, LO>;
   const int g = lane >> 2, q = lane & 3;
-  const bool hv = g < a.gq;
-  const int64_t qrow = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq + (hv ? g : 0)) * D;
-  auto qv = [&](int c) { return hv ? load_q(a, qrow + c) : 0.f; };
+  auto qv = [&](int c) { return qraw[g * C::QS + c]; };
   auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
   auto put = [&](int f, uint64_t v) { qtab[f * 32 + lane] = v; };
 #pragma unroll
@@ -810,8 +839,24 @@ __device__ __forceinline__ void prime_piece(const DecodeArgs& a, const Unit& u, 
 #else
 #define KVMIX_FUSED_BOUNDS __launch_bounds__(NW * 32, KVMIX_MINB)
 #endif
+#ifdef KVMIX_CTA_TIMES
+__device__ unsigned long long g_cta_times[4096][16];  // start, waited, end, smid, then per piece (<3): begin, q table, loop end, merged
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 template <int D, bool COMPUTE = true, bool MEMORY = true, bool LO = false, bool APPEND = false>
 __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
+#ifdef KVMIX_CTA_TIMES
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_cta_times[blockIdx.x][0] = gtimer();
+    g_cta_times[blockIdx.x][3] = smid;
+  }
+#endif
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[NW][STAGES];
@@ -833,7 +878,15 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
 
   const int piece_end = a.cta_ptr[blockIdx.x + 1];
   bool primed = false;  // the piece's first tiles were issued while the previous piece merged
+#ifdef KVMIX_CTA_TIMES
+  int dbg_k = 0;
+#define KVMIX_STAMP(j) \
+  if (threadIdx.x == 0 && blockIdx.x < 4096 && dbg_k < 3) g_cta_times[blockIdx.x][4 + 4 * dbg_k + (j)] = gtimer();
+#else
+#define KVMIX_STAMP(j)
+#endif
   for (int piece = a.cta_ptr[blockIdx.x]; piece < piece_end; ++piece) {
+  KVMIX_STAMP(0)
   const Unit u = load_unit(a, piece);
   const int ntiles = u.thi - u.tlo;
   const int nmine = ntiles > warp ? (ntiles - warp + NW - 1) / NW : 0;
@@ -881,10 +934,17 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   if (!waited) {
     pdl_wait();
     waited = true;
+#ifdef KVMIX_CTA_TIMES
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_cta_times[blockIdx.x][1] = gtimer();
+#endif
   }
   uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + NW * STAGES * C::BUF);
-  if (warp == 0) build_qtab<D, LO>(a, u, qtab, lane);
+  float* qraw = reinterpret_cast<float*>(smem + NW * STAGES * C::BUF + C::QTAB + (C::MERGE_IN_RING ? 0 : C::MERGE));
+  stage_q<D>(a, u, qraw);
   __syncthreads();
+  if (warp == 0) build_qtab<D, LO>(qraw, qtab, lane);
+  __syncthreads();
+  KVMIX_STAMP(1)
   const QFrag<D, LO> qf{qtab + lane};
 
   Acc<D> acc;
@@ -994,6 +1054,7 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   }
 #endif
 
+  KVMIX_STAMP(2)
   // ---- the next piece's first tiles stream in while this one merges (the ring is idle) ----
   if (MEMORY && !C::MERGE_IN_RING && piece + 1 < piece_end) {
     prime_piece<D>(a, load_unit(a, piece + 1), warp, lane, ring, bars, stage);
@@ -1015,7 +1076,14 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   }
   finish_piece<D>(a, u, sm_m, sm_l, sm_acc, &sm_flag);
   __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
+  KVMIX_STAMP(3)
+#ifdef KVMIX_CTA_TIMES
+  ++dbg_k;
+#endif
   }
+#ifdef KVMIX_CTA_TIMES
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_cta_times[blockIdx.x][2] = gtimer();
+#endif
 }
 
 // ====================================================================================
@@ -1040,7 +1108,7 @@ template <int D>
 struct WsCfg {
   static constexpr int SLOT = Cfg<D>::BUF + PAREA;
   static constexpr int RING = NPAIR * WSTAGES * SLOT;
-  static constexpr int SMEM = RING + (D / 8 + 2) * 32 * 8 * 2;  // rings + q fragment table (LO size)
+  static constexpr int SMEM = RING + (D / 8 + 2) * 32 * 8 * 2 + Cfg<D>::QRAW;  // rings + q table (LO size) + raw q
 };
 
 template <int D, bool LO>
@@ -1075,7 +1143,10 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
     const int ntiles = u.thi - u.tlo;
     const int nmine = ntiles > pair ? (ntiles - pair + NPAIR - 1) / NPAIR : 0;
     auto tile_of = [&](int k) { return u.tlo + pair + k * NPAIR; };
-    if (warp == 0) build_qtab<D, LO>(a, u, qtab, lane);
+    float* qraw = reinterpret_cast<float*>(smem + W::RING + (D / 8 + 2) * 32 * 8 * 2);
+    stage_q<D>(a, u, qraw);
+    __syncthreads();
+    if (warp == 0) build_qtab<D, LO>(qraw, qtab, lane);
     __syncthreads();
 
     if (is_qk) {
@@ -1322,6 +1393,12 @@ __global__ void merge_partials_kernel(const float* __restrict__ acc, const float
 }  // namespace kvmix
 
 using namespace kvmix;
+
+#ifdef KVMIX_CTA_TIMES
+extern "C" int kvmix_debug_cta_times(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_cta_times, sizeof(unsigned long long) * 16 * n) == cudaSuccess ? 0 : -5;
+}
+#endif
 
 extern "C" int kvmix_merge_partials(const float* acc, const float* lse, const float* mx, int64_t n, int64_t d,
                                     float* out, void* stream) {
