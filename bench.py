@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--int2-frac", type=float, default=None, help="override: i.i.d. bits with this INT2 fraction")
     ap.add_argument("--ctas-per-sm", type=int, default=3, help="stream-K planner: resident CTAs per SM")
     ap.add_argument("--int4-weight", type=float, default=0.9, help="stream-K planner: cost weight of INT4 bytes")
+    ap.add_argument("--tier-skew", type=float, default=None, help="stream-K planner: residency-tier cost skew")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the K1 quantize+pack (cfg3 slice) measurement")
@@ -268,7 +269,8 @@ def build_workload(args, device, rank: int):
         pool.partition(table)
         rids.append(rid)
     torch.cuda.synchronize()
-    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq, ctas_per_sm=args.ctas_per_sm, int4_weight=args.int4_weight)
+    pk = {} if args.tier_skew is None else {"tier_skew": args.tier_skew}
+    batch = kv.DecodeBatch(pool, rids, n_q_heads=Hq, ctas_per_sm=args.ctas_per_sm, int4_weight=args.int4_weight, **pk)
     q = torch.randn((L, B, Hq, d), device=device, generator=gen).to(torch.bfloat16)
     out = torch.empty_like(q)
     return pool, batch, q, out, bits

@@ -92,6 +92,7 @@ class DecodeBatch:
             if pool.device is not None and pool.device.type == "cuda":
                 n_sm = torch.cuda.get_device_properties(pool.device).multi_processor_count
             kw["n_cta"] = n_sm * int(kw.pop("ctas_per_sm", CTAS_PER_SM))
+            kw["n_sm"] = n_sm
         else:
             kw.pop("ctas_per_sm", None)
         work, cta_ptr, n_parts = plan_stream(t["n_pages"], t["n_int4"], cfg.n_kv_heads, pool.page_stride,

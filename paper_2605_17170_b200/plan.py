@@ -30,13 +30,19 @@ def _tile_bytes(n_pages: int, n_int4: int, page_stride: int, slot_stride: int, i
 
 
 def plan_stream(n_pages, n_int4, n_kv_heads: int, page_stride: int, slot_stride: int,
-                n_cta: int = 3 * NUM_SMS_B200, int4_weight: float = 0.9):
+                n_cta: int = 3 * NUM_SMS_B200, int4_weight: float = 0.9, tier_skew: float = 0.0,
+                n_sm: int = NUM_SMS_B200):
     """Return (work int32 [n_pieces, 8], cta_ptr int32 [n_cta + 1], n_parts).
 
     work rows: (unit = b*Hkv + kvh, tile_lo, tile_hi, slot, part0, nparts, 0, 0); slot is
     -1 when the piece covers its whole unit, else the partial slot (a split unit's pieces
     use slots part0 .. part0 + nparts - 1).  CTA i runs pieces cta_ptr[i] .. cta_ptr[i+1]
     in order; a CTA may hold pieces of several short units, or none.
+
+    tier_skew: CTAs i*n_sm .. (i+1)*n_sm - 1 form residency tier i (the block scheduler puts
+    tier i as the (i+1)-th CTA on every SM, and the warp schedulers favour older CTAs, so
+    lower tiers run faster, measured with tools/cta_order.py).  Tier i's cost share is
+    scaled by 1 + tier_skew * (1 - 2 i / (tiers - 1)): lower tiers get more work.
     """
     n_pages = np.asarray(n_pages, dtype=np.int64)
     n_int4 = np.asarray(n_int4, dtype=np.int64)
@@ -53,7 +59,10 @@ def plan_stream(n_pages, n_int4, n_kv_heads: int, page_stride: int, slot_stride:
     total_tiles = int(ustart[-1])
     cum = np.cumsum(np.concatenate([np.tile(t, H) for t in per_req]))
     n_cta = int(max(1, min(n_cta, total_tiles)))
-    target = cum[-1] * np.arange(1, n_cta) / n_cta
+    tiers = -(-n_cta // max(1, int(n_sm)))
+    tier = np.arange(n_cta) // max(1, int(n_sm))
+    w = 1.0 + (tier_skew * (1.0 - 2.0 * tier / (tiers - 1)) if tiers > 1 else np.zeros(n_cta))
+    target = cum[-1] * np.cumsum(w)[:-1] / w.sum()
     idx = np.searchsorted(cum, target, side="left")  # cum[idx] >= target
     prev = np.where(idx > 0, cum[np.maximum(idx - 1, 0)], 0.0)
     cuts = np.where(cum[idx] - target < target - prev, idx + 1, idx)  # nearest tile boundary

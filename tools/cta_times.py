@@ -20,7 +20,11 @@ pool, batch, q, out, bits = bench.build_workload(args, dev, 0)
 for layer in range(4):
     kv.flash_decode_batched(q[layer], batch, layer, out=out[layer])
 torch.cuda.synchronize()
-kv.flash_decode_batched(q[5], batch, 5, out=out[5])
+if os.environ.get("CTA_PIPELINED"):  # steady state: 8 back-to-back launches (PDL), the last one recorded
+    for layer in range(8, 16):
+        kv.flash_decode_batched(q[layer], batch, layer, out=out[layer])
+else:
+    kv.flash_decode_batched(q[5], batch, 5, out=out[5])
 torch.cuda.synchronize()
 n = batch.n_cta
 buf = (ctypes.c_ulonglong * (16 * n))()
