@@ -1251,7 +1251,7 @@ template <int D>
 __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs a) {
   constexpr int CPL = D / 32;
   __shared__ float qs[8][D];
-  __shared__ float sm_acc[NW * 8 * D];
+  extern __shared__ __align__(16) float sm_acc[];  // [NW * 8 * D] (dynamic: NW may be large)
   __shared__ float sm_m[NW * 8], sm_l[NW * 8];
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   __shared__ int sm_flag;
@@ -1335,7 +1335,7 @@ __global__ void __launch_bounds__(NW * 32) decode_simple_kernel(const DecodeArgs
 
 template <typename Kern>
 static int launch_kernel(Kern kern, const DecodeArgs& a, int64_t n_cta, int smem, cudaStream_t s, int nwarps = NW) {
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {  // opt in above the default 48 KB, static shared memory included
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return fail(KVMIX_ECUDA, cudaGetErrorString(e));
   }
@@ -1371,7 +1371,7 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
     case 4:
       if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_ws_kernel<D, true>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
       return launch_kernel(decode_ws_kernel<D, false>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
-    case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, 0, s);
+    case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, NW * 8 * D * (int)sizeof(float), s);
     case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
     case 3: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
     default: return fail(KVMIX_EINVAL, "bad variant");
