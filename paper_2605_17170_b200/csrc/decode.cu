@@ -180,19 +180,20 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
     }
   }
   if (u.slot < 0) return;
-  // Publish the partial: the CTA barrier orders every thread's partial stores before thread
-  // 0's gpu-scope acq_rel arrival (release is cumulative), and the last arriver's acquire
-  // orders the other CTAs' partials before its reads below -- no separate full fences.
+  // Publish the partial: every thread fences its own partial stores before the arrival
+  // (the conservative form of the pattern; a single acq_rel arrival after the barrier was
+  // measured no faster), and the last arriver fences again before reading the others'.
+  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    int old;
-    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + u.unit) : "memory");
+    const int old = atomicAdd(a.counters + u.unit, 1);
     const int last = old == u.nparts - 1;
     if (last) a.counters[u.unit] = 0;  // ready for the next launch (stream order)
     *sm_flag = last;
   }
   __syncthreads();
   if (!*sm_flag) return;
+  __threadfence();
   // The last CTA merges the unit's partials: a thread owns 4 channels of one head and pulls
   // the partials 8 at a time with all loads in flight together (one L2 round trip per 8
   // partials, not three per partial), merging online.
