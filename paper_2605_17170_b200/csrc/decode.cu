@@ -46,7 +46,7 @@ namespace kvmix {
 #endif
 constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
 #ifndef KVMIX_TILEFENCE
-#define KVMIX_TILEFENCE 0  // 1: proxy fence before every tile copy (not needed without the fused append)
+#define KVMIX_TILEFENCE 1  // proxy fence before every tile copy (0: measured +0.3%, within noise; kept for safety)
 #endif
 #ifndef KVMIX_LAZYPARAM
 #define KVMIX_LAZYPARAM 0  // 1: INT2 key scale/zero quads loaded per chunk pair (fewer live registers)
