@@ -260,6 +260,27 @@ def test_plan_cost_balance(w4):
     assert per_cta.max() / per_cta.mean() < 1.02 and per_cta.min() / per_cta.mean() > 0.98
 
 
+def test_plan_tier_skew_shares():
+    """tier_skew scales residency tier i's cost share by 1 + skew (1 - 2 i / (tiers - 1)),
+    still covering every tile exactly once."""
+    npg, n4 = np.array([1000] * 16), np.array([6000] * 16)
+    work, cta_ptr, _ = plan_stream(npg, n4, 8, 3072, 160, n_cta=444, int4_weight=1.0, tier_skew=0.1, n_sm=148)
+    cost = np.asarray(_tile_bytes(1000, 6000), dtype=np.float64)
+    per_cta = np.zeros(444)
+    for c in range(444):
+        for u, lo, hi in work[cta_ptr[c]:cta_ptr[c + 1], :3]:
+            per_cta[c] += cost[lo:hi].sum()
+    tier_mean = per_cta.reshape(3, 148).mean(axis=1) / per_cta.mean()
+    assert np.allclose(tier_mean, [1.1, 1.0, 0.9], atol=0.01)
+    assert abs(per_cta.sum() - 16 * 8 * cost.sum()) < 1
+
+
+def test_route_scratch_size():
+    """K6 scratch: one total + one count per 4096-token chunk (host-only C entry point)."""
+    from paper_2605_17170_b200._lib import lib
+    assert [lib.kvmix_route_scratch_elems(n) for n in (0, 1, 4096, 4097, 131072)] == [1, 2, 2, 3, 33]
+
+
 def test_csr_tables_cpu():
     t = csr_tables([np.array([3, 1], np.int32), np.array([], np.int32)], [np.array([5]), np.array([0, 1, 2])],
                    "cpu")
