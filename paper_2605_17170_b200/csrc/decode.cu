@@ -35,16 +35,9 @@ namespace kvmix {
 #ifndef KVMIX_SPLIT
 #define KVMIX_SPLIT 0
 #endif
-#ifndef KVMIX_PAIRS
-#define KVMIX_PAIRS 0
-#endif
 #ifndef KVMIX_META2
 #define KVMIX_META2 1  // tile metadata two tiles ahead (0: one tile ahead)
 #endif
-#ifndef KVMIX_BATCHIDS
-#define KVMIX_BATCHIDS 0  // 1: INT2 page ids 32 tiles per coalesced load (measured neutral)
-#endif
-constexpr bool PAIRS = KVMIX_PAIRS;  // fused kernel: process two same-bitwidth tiles per iteration
 #ifndef KVMIX_TILEFENCE
 #define KVMIX_TILEFENCE 1  // proxy fence before every tile copy (0: measured +0.3%, within noise; kept for safety)
 #endif
@@ -300,48 +293,6 @@ __device__ __forceinline__ void softmax_p(float (&sv)[8], Softmax& st, uint32_t 
   bP[0][1] = movtrans(pack_h2(p[2], p[3]));
   bP[1][0] = movtrans(pack_h2(p[4], p[5]));
   bP[1][1] = movtrans(pack_h2(p[6], p[7]));
-}
-
-// Two tiles' logits at once (one vote, one optional rescale for 64 tokens).
-__device__ __forceinline__ void softmax_p2(float (&sv)[8], float (&sw)[8], Softmax& st, uint32_t (&bP)[2][2],
-                                           uint32_t (&bQ)[2][2], float& al0, float& al1, bool& resc) {
-  float tm0 = fmaxf(fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6])), fmaxf(fmaxf(sw[0], sw[2]), fmaxf(sw[4], sw[6])));
-  float tm1 = fmaxf(fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7])), fmaxf(fmaxf(sw[1], sw[3]), fmaxf(sw[5], sw[7])));
-  resc = __any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK);
-  if (resc) {
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      tm0 = fmaxf(tm0, __shfl_xor_sync(0xffffffffu, tm0, off));
-      tm1 = fmaxf(tm1, __shfl_xor_sync(0xffffffffu, tm1, off));
-    }
-    const float sh0 = st.init ? fmaxf(tm0, 0.f) : tm0, sh1 = st.init ? fmaxf(tm1, 0.f) : tm1;
-    al0 = st.init ? fast_exp2(-sh0) : 0.f;
-    al1 = st.init ? fast_exp2(-sh1) : 0.f;
-    st.m0 += sh0;
-    st.m1 += sh1;
-    st.init = true;
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-      sv[i] -= sh0;
-      sv[i + 1] -= sh1;
-      sw[i] -= sh0;
-      sw[i + 1] -= sh1;
-    }
-  }
-  float p[8], r[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    p[i] = fast_exp2(sv[i]);
-    r[i] = fast_exp2(sw[i]);
-  }
-  bP[0][0] = movtrans(pack_h2(p[0], p[1]));
-  bP[0][1] = movtrans(pack_h2(p[2], p[3]));
-  bP[1][0] = movtrans(pack_h2(p[4], p[5]));
-  bP[1][1] = movtrans(pack_h2(p[6], p[7]));
-  bQ[0][0] = movtrans(pack_h2(r[0], r[1]));
-  bQ[0][1] = movtrans(pack_h2(r[2], r[3]));
-  bQ[1][0] = movtrans(pack_h2(r[4], r[5]));
-  bQ[1][1] = movtrans(pack_h2(r[6], r[7]));
 }
 
 template <int D>
@@ -896,26 +847,10 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
   const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
 
-  // tile metadata: the page id (INT2 tile) or this lane's slot (INT4 tile); loaded one
-  // iteration before its copy is issued so the copy never waits on the index load
-  // INT2 page ids come 32 tiles per coalesced load (lane i: this warp's tile 32b + i), the
-  // next batch prefetched; INT4 tiles load their 32 slot ids per tile.  k only increases.
-  int ids_cur = 0, ids_nxt = 0, batch_cur = -2;
-  auto load_ids = [&](int b) -> int {
-    const int kk = 32 * b + lane, t = u.tlo + warp + kk * NW;
-    return (kk < nmine && t < u.npg) ? a.page_ids[u.pg0 + t] : 0;
-  };
+  // tile metadata: the page id (INT2 tile) or this lane's slot ids (INT4 tile), loaded two
+  // iterations before its copy is issued so the copy never waits on the index load
   auto load_meta = [&](int k) -> int {
-    if (k >= nmine) return 0;
-    const int t = u.tlo + warp + k * NW;
-    if (!KVMIX_BATCHIDS || t >= u.npg) return tile_meta(a, u, t, lane);
-    const int b = k >> 5;
-    if (b != batch_cur) {
-      ids_cur = (b == batch_cur + 1) ? ids_nxt : load_ids(b);
-      ids_nxt = load_ids(b + 1);
-      batch_cur = b;
-    }
-    return __shfl_sync(0xffffffffu, ids_cur, k & 31);
+    return k < nmine ? tile_meta(a, u, u.tlo + warp + k * NW, lane) : 0;
   };
   auto issue = [&](int k, int meta, int s) {
     issue_tile<D>(u, u.tlo + warp + k * NW, meta, ring + s * C::BUF, &bars[warp][s], lane, kv2, kv4);
@@ -957,65 +892,6 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
   Softmax st{0.f, 0.f, false};
 
-#if KVMIX_PAIRS
-  for (int k = 0; k < nmine;) {
-    const int t = u.tlo + warp + k * NW;
-    const uint8_t* buf = ring + stage * C::BUF;
-    const int stage2 = stage + 1 == STAGES ? 0 : stage + 1;
-    const uint32_t phase2 = stage + 1 == STAGES ? phase ^ 1u : phase;
-    // two same-bitwidth full tiles at once (64 tokens: more independent MMA chains, one vote)
-    const bool two = PAIRS && COMPUTE && k + 1 < nmine &&
-                     ((t + NW < u.npg) || (t >= u.npg && u.n4 - 32 * (t + NW - u.npg) >= 32));
-    if (MEMORY) mbar_wait(&bars[warp][stage], phase);
-    if (two) {
-      if (MEMORY) mbar_wait(&bars[warp][stage2], phase2);
-      const uint8_t* buf2 = ring + stage2 * C::BUF;
-      float sv[8], sw[8];
-      uint32_t bP[2][2], bQ[2][2];
-      float al0, al1;
-      bool resc;
-      if (t < u.npg) {
-        int2_qk<D, LO>(buf, qf, a.qscale, lane, st, sv);
-        int2_qk<D, LO>(buf2, qf, a.qscale, lane, st, sw);
-        softmax_p2(sv, sw, st, bP, bQ, al0, al1, resc);
-        if (resc) rescale_acc<D>(acc, al0, al1);
-        int2_pv<D>(buf, bP, lane, acc);
-        int2_pv<D>(buf2, bQ, lane, acc);
-      } else {
-        int4_qk<D, true, LO>(buf, 32, qf, a.qscale, lane, st, sv);
-        int4_qk<D, true, LO>(buf2, 32, qf, a.qscale, lane, st, sw);
-        softmax_p2(sv, sw, st, bP, bQ, al0, al1, resc);
-        if (resc) rescale_acc<D>(acc, al0, al1);
-        int4_pv<D, true>(buf, 32, bP, lane, acc);
-        int4_pv<D, true>(buf2, 32, bQ, lane, acc);
-      }
-    } else if (!COMPUTE) {
-      // measurement variant: data movement only (no dequant / MMA)
-    } else if (t < u.npg) {
-      int2_tile<D, LO>(buf, qf, a.qscale, lane, st, acc);
-    } else {
-      const int nv = min(32, u.n4 - 32 * (t - u.npg));
-      if (nv == 32) int4_tile<D, true, LO>(buf, 32, qf, a.qscale, lane, st, acc);
-      else int4_tile<D, false, LO>(buf, nv, qf, a.qscale, lane, st, acc);
-    }
-    __syncwarp();
-    const int nt = two ? 2 : 1;
-    for (int i = 0; i < nt; ++i) {
-      if (MEMORY && k + STAGES < nmine) {
-        fence_proxy_async();
-        issue(k + STAGES, meta_next, stage);
-      }
-      meta_next = meta_next2;
-      meta_next2 = load_meta(k + STAGES + 2);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
-      }
-      ++k;
-    }
-  }
-
-#else
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
     const uint8_t* buf = ring + stage * C::BUF;
@@ -1055,7 +931,6 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
       phase ^= 1u;
     }
   }
-#endif
 
   KVMIX_STAMP(2)
   // ---- the next piece's first tiles stream in while this one merges (the ring is idle) ----
