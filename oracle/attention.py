@@ -79,3 +79,63 @@ def dense_f64(q, k, v, scale=None):
     w = np.exp(logits)
     w /= w.sum(axis=2, keepdims=True)
     return np.einsum("hqn,nhd->qhd", w, v)
+
+
+def attention_full(q, k, v, scale=None, causal: bool = False):
+    """attention.py:32-64 restated: fp32 dense GQA attention, q [n_q, H, d], k/v [N, Hkv, d];
+    with ``causal`` the queries are aligned to the last n_q keys."""
+    q = np.asarray(q, dtype=np.float32)
+    k = np.asarray(k, dtype=np.float32)
+    v = np.asarray(v, dtype=np.float32)
+    n_q, H, d = q.shape
+    n = k.shape[0]
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    ratio = H // k.shape[1]
+    ke = np.repeat(k, ratio, axis=1)
+    ve = np.repeat(v, ratio, axis=1)
+    logits = np.einsum("qhd,nhd->hqn", q, ke) * np.float32(scale)
+    if causal:
+        mask = np.arange(n)[None, :] > ((n - n_q) + np.arange(n_q))[:, None]
+        logits = np.where(mask[None], -np.inf, logits)
+    logits = logits - logits.max(axis=2, keepdims=True)
+    w = np.exp(logits)
+    p = w / w.sum(axis=2, keepdims=True)
+    return np.einsum("hqn,nhd->qhd", p, ve)
+
+
+def output_mse_per_head(o_ref, o_test):
+    """attention.py:77-83: per-head mean over positions of the squared L2 error (float64)."""
+    o_ref = np.asarray(o_ref, dtype=np.float64)
+    o_test = np.asarray(o_test, dtype=np.float64)
+    return ((o_ref - o_test) ** 2).sum(axis=-1).mean(axis=0)
+
+
+def apply_mixed_quantization(k, v, row_bits, g: int = 32):
+    """attention.py:103-127: rows with bits 2 / 4 replaced by their quantize-dequantize
+    images (the pool's routing over the selected rows, codec.fake_quant_kv); 0 = untouched."""
+    from .codec import fake_quant_kv
+    k = np.array(k, dtype=np.float32)
+    v = np.array(v, dtype=np.float32)
+    bits = np.asarray(row_bits)
+    sel = np.flatnonzero(bits != 0)
+    if sel.size:
+        kq, vq = fake_quant_kv(k[sel], v[sel], bits[sel], g)
+        k[sel], v[sel] = kq, vq
+    return k, v
+
+
+def measure_raw(captures, bitwidths=(2, 4)):
+    """calibration.py:108-125 restated over the functions above."""
+    entries = {}
+    for cap in captures:
+        tags = np.asarray(cap.tags)
+        for li, lay in enumerate(cap.layers):
+            ref = attention_full(lay.q, lay.k, lay.v, causal=True)
+            for tag in sorted(set(int(t) for t in tags)):
+                for b in bitwidths:
+                    kq, vq = apply_mixed_quantization(lay.k, lay.v, np.where(tags == tag, b, 0), cap.group_len)
+                    mse = output_mse_per_head(ref, attention_full(lay.q, kq, vq, causal=True))
+                    for h, e in enumerate(mse):
+                        entries[(li, cap.request_id, h, tag, b)] = float(e)
+    return entries

@@ -16,6 +16,7 @@ from .attention import (
     flash_decode_layers_from_host,
     merge_partials,
 )
+from . import calib  # noqa: F401  (calibration replay on the GPU)
 from .errors import CapacityError, InfeasibleBudgetError, KvmixError, TemplateStructureError, ValidationError
 from .plan import plan_stream
 from .pool import (
