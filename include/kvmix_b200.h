@@ -106,6 +106,14 @@ int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int
                          int64_t offset, int64_t layer, int64_t n_kv_heads, int64_t head_dim, const int32_t* slots,
                          int64_t m, float* k_out, float* v_out, void* stream);
 
+/* K5 with a typed output: out_dtype KVMIX_F32 (== kvmix_gather_dequant), KVMIX_BF16 or KVMIX_F16
+ * (round-to-nearest image of the exact dequantized value) -- the K/V of an fp16 / bf16
+ * prefill attention over matched prefixes read straight from the pool. */
+int kvmix_gather_dequant_typed(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
+                               int64_t pool_int4, int64_t offset, int64_t layer, int64_t n_kv_heads, int64_t head_dim,
+                               const int32_t* slots, int64_t m, void* k_out, void* v_out, int32_t out_dtype,
+                               void* stream);
+
 /* ---- device-side page-table build (K6) ----------------------------------------------- */
 
 /* Scratch size (int64 elements) of the routing counts for an n-token request. */

@@ -49,6 +49,8 @@ _SIGS = {
                              _I64, _P, _P], ctypes.c_int),
     "kvmix_append_int4": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P], ctypes.c_int),
     "kvmix_gather_dequant": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P], ctypes.c_int),
+    "kvmix_gather_dequant_typed": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P],
+                                   ctypes.c_int),
     "kvmix_flash_decode": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                             _P, _P, _I64, _P, _P, _F, _I32, _P], ctypes.c_int),
     "kvmix_flash_decode_append": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P,

@@ -465,12 +465,19 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
   }
 }
 
-// K5 gather-dequant (pool.py:394-439): thread per (slot, head, channel) -> f32 k/v.
-template <int D>
+template <typename TO> __device__ __forceinline__ TO from_f32(float x);
+template <> __device__ __forceinline__ float from_f32<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ __half from_f32<__half>(float x) { return __float2half_rn(x); }
+
+// K5 gather-dequant (pool.py:394-439): thread per (slot, head, channel) -> k/v in TO (f32 is
+// the reference's exact dequantized value; bf16 / f16 are its round-to-nearest image, the
+// input of an fp16 / bf16 prefill attention over the pool).
+template <int D, typename TO>
 __global__ void gather_dequant_kernel(const uint8_t* __restrict__ int2_pool, const uint8_t* __restrict__ int4_pool,
                                       int64_t pool_pages, int64_t pool_int4, int64_t offset, int64_t layer,
                                       int64_t n_kv_heads, const int32_t* __restrict__ slots, int64_t m,
-                                      float* __restrict__ k_out, float* __restrict__ v_out) {
+                                      TO* __restrict__ k_out, TO* __restrict__ v_out) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= m * n_kv_heads * D) return;
   const int c = (int)(idx % D);
@@ -498,8 +505,8 @@ __global__ void gather_dequant_kernel(const uint8_t* __restrict__ int2_pool, con
     const uint32_t vc = (rec[SL_VC(D) + sl_vc_off(D, c >> 1)] >> sh) & 15u;
     vv = __fmaf_rn((float)vc, half_at(rec + SL_VS(D), c / G), half_at(rec + SL_VZ(D), c / G));
   }
-  k_out[idx] = kv;
-  v_out[idx] = vv;
+  k_out[idx] = from_f32<TO>(kv);
+  v_out[idx] = from_f32<TO>(vv);
 }
 
 }  // namespace kvmix
@@ -710,13 +717,42 @@ extern "C" int kvmix_append_int4(const void* k, const void* v, int32_t dtype, in
   }
 }
 
+template <typename TO>
+static int launch_gather(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4,
+                         int64_t offset, int64_t layer, int64_t H, int64_t d, const int32_t* slots, int64_t m,
+                         void* k_out, void* v_out, cudaStream_t s) {
+  const int64_t total = m * H * d;
+  const unsigned grid = (unsigned)((total + 255) / 256);
+  DISPATCH_D(d, gather_dequant_kernel<D, TO><<<grid, 256, 0, s>>>(int2_pool, int4_pool, pool_pages, pool_int4, offset,
+                                                                   layer, H, slots, m, static_cast<TO*>(k_out),
+                                                                   static_cast<TO*>(v_out)));
+  return check_launch("gather_dequant");
+}
+
+extern "C" int kvmix_gather_dequant_typed(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
+                                          int64_t pool_int4, int64_t offset, int64_t layer, int64_t H, int64_t d,
+                                          const int32_t* slots, int64_t m, void* k_out, void* v_out,
+                                          int32_t out_dtype, void* stream) {
+  if (m == 0) return KVMIX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (out_dtype) {
+    case KVMIX_F32:
+      return launch_gather<float>(int2_pool, int4_pool, pool_pages, pool_int4, offset, layer, H, d, slots, m, k_out,
+                                  v_out, s);
+    case KVMIX_BF16:
+      return launch_gather<__nv_bfloat16>(int2_pool, int4_pool, pool_pages, pool_int4, offset, layer, H, d, slots, m,
+                                          k_out, v_out, s);
+    case KVMIX_F16:
+      return launch_gather<__half>(int2_pool, int4_pool, pool_pages, pool_int4, offset, layer, H, d, slots, m, k_out,
+                                   v_out, s);
+    default:
+      return fail(KVMIX_EINVAL, "unsupported output dtype");
+  }
+}
+
 extern "C" int kvmix_gather_dequant(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
                                     int64_t pool_int4, int64_t offset, int64_t layer, int64_t H, int64_t d,
                                     const int32_t* slots, int64_t m, float* k_out, float* v_out, void* stream) {
-  if (m == 0) return KVMIX_OK;
-  int64_t total = m * H * d;
-  unsigned grid = (unsigned)((total + 255) / 256);
-  DISPATCH_D(d, gather_dequant_kernel<D><<<grid, 256, 0, (cudaStream_t)stream>>>(
-                    int2_pool, int4_pool, pool_pages, pool_int4, offset, layer, H, slots, m, k_out, v_out));
-  return check_launch("gather_dequant");
+  return kvmix_gather_dequant_typed(int2_pool, int4_pool, pool_pages, pool_int4, offset, layer, H, d, slots, m, k_out,
+                                    v_out, KVMIX_F32, stream);
 }

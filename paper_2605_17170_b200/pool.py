@@ -392,6 +392,27 @@ class MixedPrecisionPool:
         if not (np.all(ok2) and np.all(ok4)):
             raise ValidationError("slot read before write")
 
+    def gather_device(self, slots, layer: int, dtype=torch.float32):
+        """K5 on the device: k, v [m, Hkv, d] of ``slots`` (one layer) in ``dtype`` (f32: the
+        exact dequantized values; bf16 / f16: their round-to-nearest images, ready for an
+        fp16 / bf16 prefill attention over the pool).  Liveness and write checks as read_slot."""
+        cfg = self.config
+        s = np.asarray(slots, dtype=np.int64)
+        if s.size and (s.min() < 0 or s.max() >= cfg.total_slots or np.any(self._owner[s] < 0)):
+            raise ValidationError("gather of a slot that is not live")
+        if not 0 <= layer < cfg.n_layers:
+            raise ValidationError(f"layer {layer} out of range")
+        self._require_written(s, layer)
+        m = s.size
+        sl = torch.as_tensor(s.astype(np.int32), device=self.device)
+        k = torch.empty((m, cfg.n_kv_heads, cfg.head_dim), dtype=dtype, device=self.device)
+        v = torch.empty_like(k)
+        _lib.check(lib.kvmix_gather_dequant_typed(
+            self.int2_pool.data_ptr(), self.int4_pool.data_ptr(), self.n_pages, self.n_int4, cfg.offset, layer,
+            cfg.n_kv_heads, cfg.head_dim, sl.data_ptr(), m, k.data_ptr(), v.data_ptr(), _lib.dtype_code(k),
+            _lib.stream()))
+        return k, v
+
     def _gather_dev(self, slots: np.ndarray, layer: int):
         cfg = self.config
         m = slots.size

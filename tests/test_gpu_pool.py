@@ -295,3 +295,30 @@ def test_alloc_device_errors(cuda):
     pool.free("a")
     assert len(t) == 64
     pool.check_invariants()
+
+
+def test_gather_device_typed(cuda):
+    """K5 with bf16 / f16 output (kvmix_gather_dequant_typed) is the round-to-nearest image of
+    the exact f32 dequantized values; dead or unwritten slots are rejected like read_slot."""
+    L, H, d = 2, 2, 128
+    cfg = kv.PoolConfig(total_slots=2000, offset=1024, n_layers=L, n_kv_heads=H, head_dim=d)
+    pool = kv.MixedPrecisionPool(cfg)
+    rng = np.random.default_rng(77)
+    n = 600
+    bits = rng.choice([2, 4], size=n, p=[0.75, 0.25])
+    k, v = rand_kv(77, L, n, H, d)
+    t = pool.alloc("r", bits)
+    pool.write_prefill(t, k, v)
+    for layer in range(L):
+        k32, v32 = pool.gather_device(t.slots, layer)
+        kr, vr = pool._gather_dev(t.slots, layer)
+        assert torch.equal(k32, kr) and torch.equal(v32, vr)
+        for dt in (torch.bfloat16, torch.float16):
+            kd, vd = pool.gather_device(t.slots, layer, dtype=dt)
+            assert kd.dtype == dt and torch.equal(kd, k32.to(dt)) and torch.equal(vd, v32.to(dt))
+    t2 = pool.alloc("unwritten", np.full(40, 4))
+    with pytest.raises(kv.ValidationError):
+        pool.gather_device(t2.slots, 0)
+    pool.free("r")
+    with pytest.raises(kv.ValidationError):
+        pool.gather_device(t.slots, 0)
