@@ -296,7 +296,9 @@ def _prefill_layers(pool, table, k, v, l0):
         k.data_ptr(), v.data_ptr(), _lib.dtype_code(k), k.shape[0], k.shape[1], cfg.n_kv_heads, cfg.head_dim,
         pt.data_ptr(), pi.data_ptr(), pt.shape[0], it.data_ptr(), ii.data_ptr(), t4.size,
         pool.int2_pool.data_ptr() + lh * pool.n_pages * pool.page_stride, pool.n_pages,
-        pool.int4_pool.data_ptr() + lh * pool.n_int4 * pool.slot_stride, pool.n_int4, None, _lib.stream()))
+        pool.int4_pool.data_ptr() + lh * pool.n_int4 * pool.slot_stride, pool.n_int4, pool.status.data_ptr(),
+        _lib.stream()))
+    pool._written = True
     pool._page_written[l0:l0 + k.shape[0], :, s[t2[::g]] // g] = True
     pool._int4_written[l0:l0 + k.shape[0], :, s[t4] - cfg.offset] = True
 

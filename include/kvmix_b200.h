@@ -82,11 +82,23 @@ int kvmix_unpack_codes(const uint8_t* packed, int64_t n, int32_t bitwidth, uint8
 
 /* ---- pool data plane ------------------------------------------------------------- */
 
+/* Pool status words (device int32[KVMIX_POOL_STATUS_WORDS], owned by the pool, zeroed at
+ * creation): the pool writers (kvmix_write_prefill, kvmix_append_int4, the fused decode
+ * append) set bit 0 of word ERR on non-finite input and raise KSCALE / VSCALE to the
+ * largest INT2 key-page scale / V scale (INT2 and INT4) they stored, as fp32 bit patterns
+ * (atomicMax; non-negative floats order like their bits).  The decode kernel reads the two
+ * scales to bound its fp16 operands (q * s_k and p * s_v) without per-tile checks. */
+#define KVMIX_POOL_STATUS_WORDS 4
+#define KVMIX_POOL_STATUS_ERR 0
+#define KVMIX_POOL_STATUS_KSCALE 1
+#define KVMIX_POOL_STATUS_VSCALE 2
+
 /* Replaces pool.py:228 MixedPrecisionPool.write_prefill (with write_page :201 and the INT4
  * branch :253-262): quantize+pack one request's prefill K/V [L][n_tokens][Hkv][d]
  * (dtype KVMIX_F32/BF16/F16, contiguous) into the pools.
  * page_tokens [n_req_pages][G]: token index of each page row (token order);
- * page_ids [n_req_pages]: destination page index; int4_tokens/int4_ids [n_req_int4]. */
+ * page_ids [n_req_pages]: destination page index; int4_tokens/int4_ids [n_req_int4].
+ * err_flag: the pool status words (KVMIX_POOL_STATUS_*), may be NULL. */
 int kvmix_write_prefill(const void* keys, const void* values, int32_t dtype, int64_t n_layers, int64_t n_tokens,
                         int64_t n_kv_heads, int64_t head_dim, const int32_t* page_tokens, const int32_t* page_ids,
                         int64_t n_req_pages, const int32_t* int4_tokens, const int32_t* int4_ids,
@@ -95,7 +107,8 @@ int kvmix_write_prefill(const void* keys, const void* values, int32_t dtype, int
 
 /* Replaces pool.py:284 append_decode_token (data half; the host pops the slot) and
  * pool.py:217 write_token: quantize n tokens' K/V [n][n_layers_in][Hkv][d] at INT4 into
- * int4 indices int4_ids[n], pool layers [layer0, layer0 + n_layers_in). */
+ * int4 indices int4_ids[n], pool layers [layer0, layer0 + n_layers_in).
+ * err_flag: the pool status words (KVMIX_POOL_STATUS_*), may be NULL. */
 int kvmix_append_int4(const void* k, const void* v, int32_t dtype, int64_t n, int64_t n_layers_in, int64_t layer0,
                       int64_t n_layers, int64_t n_kv_heads, int64_t head_dim, const int32_t* int4_ids,
                       uint8_t* int4_pool, int64_t pool_int4, int32_t* err_flag, void* stream);
@@ -157,15 +170,24 @@ int kvmix_route_tokens(const int8_t* bits, int64_t n, int32_t page_size, const i
  *     of the batch, see plan.py); the last CTA to finish a split unit merges its partials.
  *   counters [batch * Hkv] int32, zero before the first launch; every launch leaves them zero.
  *   variant: 0 = tensor-core kernel (mma.sync m16n8k16; plan with 3 CTAs per SM), 1 = simple
- *     CUDA-core kernel, 2 = data movement only, 3 = compute only on stale smem (measurement;
- *     output meaningless), 4 = warp-specialised tensor-core kernel (plan with 2 CTAs per SM)
+ *     CUDA-core kernel; measurement builds (-DKVMIX_MEASURE_VARIANTS) add 2 = data movement
+ *     only, 3 = compute only on stale smem (output meaningless), 4 = warp-specialised
+ *     tensor-core kernel (plan with 2 CTAs per SM)
+ *   pool_status: the pool status words (KVMIX_POOL_STATUS_*); NULL = operand bounds unknown
+ *     (exact-max softmax and q pre-scaled for the largest finite scales: correct, slower).
+ *   flags: KVMIX_DECODE_POOL_WRITTEN when a kernel that wrote this pool (write_prefill,
+ *     append_int4, ...) precedes the launch in the stream: the kernel then waits for it before
+ *     its first KV copies (otherwise they overlap the previous kernel's tail through
+ *     programmatic dependent launch).
  * Requires n_q_heads % Hkv == 0 and n_q_heads / Hkv <= 8, d in {32, 64, 128}. */
+#define KVMIX_DECODE_POOL_WRITTEN 1
 int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dtype, const uint8_t* int2_pool,
                        const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
                        int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
                        const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
                        const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
-                       float* partials, int32_t* counters, float scale, int32_t variant, void* stream);
+                       float* partials, int32_t* counters, float scale, int32_t variant, int32_t* pool_status,
+                       int32_t flags, void* stream);
 
 /* K4 fused decode append (pool.py:284-306 append_decode_token data half + attention.py:175
  * flash_decode, one launch): the same as kvmix_flash_decode (variant 0) for one layer, where
@@ -179,7 +201,7 @@ int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* out, int32_t
                               const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
                               const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
                               float* partials, int32_t* counters, float scale, const void* k_new, const void* v_new,
-                              int32_t kv_dtype, void* stream);
+                              int32_t kv_dtype, int32_t* pool_status, int32_t flags, void* stream);
 
 /* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
  * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */

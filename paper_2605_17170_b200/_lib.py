@@ -52,9 +52,9 @@ _SIGS = {
     "kvmix_gather_dequant_typed": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P],
                                    ctypes.c_int),
     "kvmix_flash_decode": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
-                            _P, _P, _I64, _P, _P, _F, _I32, _P], ctypes.c_int),
+                            _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
     "kvmix_flash_decode_append": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P,
-                                   _P, _P, _P, _I64, _P, _P, _F, _P, _P, _I32, _P], ctypes.c_int),
+                                   _P, _P, _P, _I64, _P, _P, _F, _P, _P, _I32, _P, _I32, _P], ctypes.c_int),
     "kvmix_merge_partials": ([_P, _P, _P, _I64, _I64, _P, _P], ctypes.c_int),
     "kvmix_route_scratch_elems": ([_I64], _I64),
     "kvmix_count_int2": ([_P, _I64, _P, _P, _P], ctypes.c_int),
@@ -74,6 +74,9 @@ for _name, (_args, _ret) in _SIGS.items():
 EXPORTED = tuple(_SIGS)
 
 F32, BF16, F16 = 0, 1, 2
+POOL_STATUS_WORDS = 4          # kvmix_b200.h KVMIX_POOL_STATUS_*
+POOL_STATUS_ERR, POOL_STATUS_KSCALE, POOL_STATUS_VSCALE = 0, 1, 2
+DECODE_POOL_WRITTEN = 1        # kvmix_b200.h KVMIX_DECODE_POOL_WRITTEN
 _DT = {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}
 
 

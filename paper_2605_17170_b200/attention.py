@@ -139,13 +139,21 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
         raise ValidationError(f"q must be [{batch.batch}, {batch.n_q_heads}, {cfg.head_dim}]")
     if not 0 <= layer < cfg.n_layers:
         raise ValidationError("layer out of range")
+    if q.device != pool.device:
+        raise ValidationError(f"q must be on the pool's device {pool.device}")
     if not q.is_contiguous():
         q = q.contiguous()
     if out is None:
         out = torch.empty_like(q)
+    elif (tuple(out.shape) != tuple(q.shape) or not out.is_contiguous() or out.device != pool.device
+          or out.dtype not in (torch.float32, torch.bfloat16, torch.float16)):
+        raise ValidationError(f"out must be a contiguous f32/bf16/f16 [{batch.batch}, {batch.n_q_heads}, "
+                              f"{cfg.head_dim}] tensor on {pool.device}")
     if scale is None:
         scale = 1.0 / math.sqrt(cfg.head_dim)
     t = batch.csr
+    # a pool writer launched just before may still be storing what this launch prefetches
+    flags = _lib.DECODE_POOL_WRITTEN if pool._written is True or pool._written == layer else 0
     if append is not None:
         k_new, v_new = append
         want = (batch.batch, cfg.n_kv_heads, cfg.head_dim)
@@ -155,6 +163,16 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
             raise ValidationError("the fused decode append runs in the tensor-core kernel")
         if np.any(t["n_int4"] == 0):
             raise ValidationError("every request needs a reserved INT4 slot for the fused append")
+        if batch.last_int4 is None:
+            raise ValidationError("the fused append needs a DecodeBatch built from request_ids")
+        # the newest INT4 entry of every table must be a slot reserved for this step and not
+        # yet written at this layer (reserve_decode_slots, then batch.refresh())
+        last = np.array([int(pool.table(r).slots[-1]) for r in batch.request_ids], dtype=np.int64)
+        if not np.array_equal(last, batch.last_int4):
+            raise ValidationError("page tables changed since batch.refresh(): refresh before the fused append")
+        if np.any(pool._int4_written[layer, :, last - cfg.offset]):
+            raise ValidationError("the newest slot is already written at this layer: reserve_decode_slots "
+                                  "and batch.refresh() before the fused append")
         k_new = k_new.contiguous()
         v_new = v_new.to(k_new.dtype).contiguous()
         _lib.check(lib.kvmix_flash_decode_append(
@@ -163,9 +181,9 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
             batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
             t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
             batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), k_new.data_ptr(),
-            v_new.data_ptr(), _lib.dtype_code(k_new), _lib.stream()))
-        if batch.last_int4 is not None:
-            pool._int4_written[layer, :, batch.last_int4 - cfg.offset] = True
+            v_new.data_ptr(), _lib.dtype_code(k_new), pool.status.data_ptr(), flags, _lib.stream()))
+        pool._int4_written[layer, :, batch.last_int4 - cfg.offset] = True
+        pool._written = layer  # the fused append stored this layer's new token
         return out
     _lib.check(lib.kvmix_flash_decode(
         q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
@@ -173,7 +191,8 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
         batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
         t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
         batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), int(variant),
-        _lib.stream()))
+        pool.status.data_ptr(), flags, _lib.stream()))
+    pool._written = False
     return out
 
 

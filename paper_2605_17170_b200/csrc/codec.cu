@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     }
   };
   int stg = 0;
+  float kmx = 0.f, vmx = 0.f;  // largest key-page / V scales this thread stored (pool status)
   if (blockIdx.x < n_items) {
     rows(blockIdx.x, 0);
     __syncthreads();
@@ -377,6 +378,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
       for (int i = 0; i < G; ++i) x[i] = load_one<D, T>(Ks, i, c);
       uint32_t w[2], pz;
       encode_group<2>(x, w, pz, err);
+      kmx = fmaxf(kmx, scale_of(pz));
 #pragma unroll
       for (int b = 0; b < 8; ++b) srec[pg_kc_off(D, b, c)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
       reinterpret_cast<uint16_t*>(srec + PG_KS(D))[pg_kp_idx(D, c)] = (uint16_t)(pz & 0xffffu);
@@ -389,6 +391,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
       load_row_group<D, T>(Vs, t, j, x);  // 16-byte loads; rows t % 8 of a quarter warp differ: no conflicts
       uint32_t w[2], pz;
       encode_group<2>(x, w, pz, err);
+      vmx = fmaxf(vmx, scale_of(pz));
 #pragma unroll
       for (int b = 0; b < 8; ++b)
         srec[PG_VC(D) + pg_vc_off(D, t, 8 * j + b)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
@@ -403,6 +406,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     __syncthreads();  // srec and this stage are free
   }
   cp_async_wait<0>();
+  publish_scales(err, kmx, vmx);
 }
 
 // this lane's D/32 consecutive elements, one vector load when they fill 8 or 16 bytes
@@ -450,11 +454,13 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
   __syncwarp();
   const int tw = lane / NG, j = lane % NG;
   const int64_t i = i0 + tw;
+  float vmx = 0.f;
   if (i < n) {
     const int64_t t = tokens ? tokens[i] : i;
     const int64_t base = l * layer_stride + t * tok_stride + (int64_t)h * D + 32 * j;
-    encode_int4_group<D, T>(keys + base, values + base, st + tw * SS, nullptr, j, err);
+    vmx = encode_int4_group<D, T>(keys + base, values + base, st + tw * SS, nullptr, j, err);
   }
+  publish_scales(err, 0.f, vmx);
   __syncwarp();
   const int nt = (int)min((int64_t)TPW, n - i0);
   for (int c = lane; c < nt * (SS / 16); c += 32) {

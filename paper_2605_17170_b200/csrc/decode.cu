@@ -42,7 +42,7 @@ namespace kvmix {
 #define KVMIX_TILEFENCE 1  // proxy fence before every tile copy (0: measured +0.3%, within noise; kept for safety)
 #endif
 #ifndef KVMIX_LAZYPARAM
-#define KVMIX_LAZYPARAM 0  // 1: INT2 key scale/zero quads loaded per chunk pair (fewer live registers)
+#define KVMIX_LAZYPARAM 1  // 1: INT2 key scale/zero quads loaded per chunk pair (fewer live registers)
 #endif
 #ifndef KVMIX_NW
 #define KVMIX_NW 4
@@ -50,7 +50,13 @@ namespace kvmix {
 constexpr int NW = KVMIX_NW;          // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr float LOG2E = 1.4426950408889634f;
-constexpr float RESCALE_SLACK = 8.f;  // see softmax_tile
+constexpr float RESCALE_SLACK = 8.f;  // largest lazy-rescale slack (log2 units), see softmax_p
+#ifndef KVMIX_Q2EXACT
+#define KVMIX_Q2EXACT 1  // INT2 key pages: q*s as an exact fp16 hi + lo pair (two MMAs per chunk)
+#endif
+#ifndef KVMIX_Q2ACC
+#define KVMIX_Q2ACC 1  // 1: the lo MMAs accumulate into the hi accumulators (fewer registers, longer chains)
+#endif
 
 template <int D>
 struct Cfg {
@@ -98,6 +104,11 @@ struct DecodeArgs {
   const void* app_v;
   int app_dtype;
   uint8_t* int4_pool_w;
+  // Pool status words (kvmix_b200.h KVMIX_POOL_STATUS_*): the largest INT2 key-page scale
+  // and V scale ever written bound the fp16 operands q' = q*s_k and P' = p*s_v (see
+  // Softmax::slack, build_qtab); NULL = no bound known (safe settings).
+  int32_t* pool_status;
+  int flags;  // KVMIX_DECODE_POOL_WRITTEN: wait for the previous kernel before the first KV copies
 };
 
 __device__ __forceinline__ float load_q(const DecodeArgs& a, int64_t idx) {
@@ -240,8 +251,31 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
 // zero-point MMA (Acc::zs), so it sums exactly the fp16 p the PV MMAs use.
 struct Softmax {
   float m0, m1;
-  bool init;  // false until the warp's first tile of the piece set the max
+  bool init;    // false until the warp's first tile of the piece set the max
+  float slack;  // p <= 2^slack: P' = p*s_v stays finite for every V scale of the pool
 };
+
+// Launch-wide operand bounds from the pool status words (kvmix_b200.h): with s_v < 2^(ev+1)
+// the lazy softmax may let p reach 2^slack, slack = min(8, 15 - ev), so P' = p*s_v < 2^16
+// rounds to at most 65504; with s_k < 2^(ek+1) and |q| < 2^(eq+1), q is pre-scaled by
+// 2^-qexp, qexp = max(0, eq + max(ek, 5) - 13), so q*s_k and the INT4 group sums of q
+// (<= 32|q|) stay below 2^15 (build_qtab).  Unknown bounds (NULL) = the largest finite.
+__device__ __forceinline__ int ilog2f(float x) { return ((__float_as_int(x) >> 23) & 0xff) - 127; }
+struct Bounds {
+  float slack;
+  int ek;
+};
+__device__ __forceinline__ Bounds pool_bounds(const int32_t* st) {
+  float kmax = 65504.f, vmax = 65504.f;
+  if (st != nullptr) {
+    kmax = __int_as_float(__ldcg(st + KVMIX_POOL_STATUS_KSCALE));
+    vmax = __int_as_float(__ldcg(st + KVMIX_POOL_STATUS_VSCALE));
+  }
+  Bounds b;
+  b.slack = (float)max(0, min((int)RESCALE_SLACK, 15 - ilog2f(fmaxf(vmax, 1.f))));
+  b.ek = max(ilog2f(fmaxf(kmax, 1.f)), 5);
+  return b;
+}
 
 template <int D>
 struct Acc {
@@ -256,16 +290,16 @@ __device__ __forceinline__ uint32_t ld_s32(const uint8_t* base, int off) {
 
 // Online softmax over one 32-token tile.  sv holds the logits minus the running max;
 // returns the P^T B fragments of PV k-steps 0, 1.  Lazy rescale: the max is only raised
-// when some logit exceeds it by > RESCALE_SLACK (log2 units), so p <= 2^RESCALE_SLACK
-// stays well inside fp16 and the common path needs no cross-lane reduction -- only a
-// per-lane max and one vote.  The first tile of a piece establishes the max exactly.
+// when some logit exceeds it by > st.slack (log2 units, <= RESCALE_SLACK), so p <= 2^slack
+// stays inside fp16 (and p*s_v too, see pool_bounds) and the common path needs no
+// cross-lane reduction -- only a per-lane max and one vote.  The first tile of a piece establishes the max exactly.
 // When the max moved, `resc` is set (warp-uniform) and the accumulators must be
 // multiplied by (al0, al1) (0 on the first tile).
 __device__ __forceinline__ void softmax_p(float (&sv)[8], Softmax& st, uint32_t (&bP)[2][2], float& al0,
                                           float& al1, bool& resc) {
   float tm0 = fmaxf(fmaxf(sv[0], sv[2]), fmaxf(sv[4], sv[6]));
   float tm1 = fmaxf(fmaxf(sv[1], sv[3]), fmaxf(sv[5], sv[7]));
-  resc = __any_sync(0xffffffffu, !st.init || tm0 > RESCALE_SLACK || tm1 > RESCALE_SLACK);
+  resc = __any_sync(0xffffffffu, !st.init || tm0 > st.slack || tm1 > st.slack);
   if (resc) {
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -351,6 +385,31 @@ __device__ __forceinline__ constexpr uint32_t F2(int e) { return 0x00030003u << 
 constexpr uint32_t N4L = 0x000F000Fu, N4H = 0x00F000F0u;  // INT4 low / high nibble of bytes 0, 2
 constexpr uint32_t ONES = 0x3C003C00u;  // (1.0, 1.0) fp16
 constexpr float P24 = 16777216.f, P22 = 4194304.f, P20 = 1048576.f, P18 = 262144.f;
+constexpr float P10 = 1024.f, P8 = 256.f, P6 = 64.f, P4 = 16.f;
+// Key codes enter QK as NORMAL fp16 numbers: (field | 1.0) - 1.0 = code * 2^(p-10) for a
+// field at bit p (one LOP3 + one exact HSUB2 per two codes).  The tensor core reduces
+// products of subnormal operands with ~13 bits of precision relative to the largest
+// product of the MMA (tools/microbench/tc_precision.cu: 2^-12.3 worst, vs 2^-21.5 for
+// normal operands), which turns into logit errors that a peaked softmax amplifies; value
+// codes (PV) keep the cheaper subnormal form, where the same bound is relative to the
+// dominant term of the output.
+#ifndef KVMIX_QKNORM
+#define KVMIX_QKNORM 1
+#endif
+__device__ __forceinline__ uint32_t kcode(uint32_t v, uint32_t mask) {
+#if KVMIX_QKNORM
+  return hsub2u(lop_and_or(v, mask, ONES), ONES);
+#else
+  return v & mask;
+#endif
+}
+#if KVMIX_QKNORM
+constexpr float KF0 = P10, KF1 = P8, KF2 = P6, KF3 = P4;  // INT2 key field e at 2^(2e-10)
+constexpr float KF4 = P6;                                 // INT4 key products at 2^-6
+#else
+constexpr float KF0 = P24, KF1 = P22, KF2 = P20, KF3 = P18;
+constexpr float KF4 = P20;
+#endif
 
 // Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).
 //  b2[I]  INT2 key pages, chunk I, lane q: channels cb = q*D/4 + 4I: (cb, cb+2) / (cb+1, cb+3)
@@ -400,7 +459,7 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
     lds_vec<16>(buf + PG_KZ(D) + (4 * i + q) * 16, kzw + 4 * i);
   }
 #endif
-  // two accumulators per M tile (even / odd chunks) halve the HMMA dependency chains
+  // two accumulators per M tile (hi / lo parts of q*s) halve the HMMA dependency chains
   float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, d0[4] = {0.f, 0.f, 0.f, 0.f},
         d1[4] = {0.f, 0.f, 0.f, 0.f};
   // bias sum_c q_c z_c: the KZ quad of chunks (2P, 2P+1) is (z_2P.p0, z_2P+1.p0, z_2P.p1, z_2P+1.p1),
@@ -419,19 +478,37 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
 #endif
     const uint32_t w = kw[i], x = w >> 8;
     const uint64_t qi = qf.b2(i);
-    const uint64_t qs = pack_b64(hmul2u(lo32(qi), ksw[P4 + odd]), hmul2u(hi32(qi), ksw[P4 + 2 + odd]));
-#if KVMIX_SPLIT
-    mma16816_b64(odd ? d0 : c0, w & F2(0), w & F2(1), x & F2(0), x & F2(1), qs);
-    mma16816_b64(odd ? d1 : c1, w & F2(2), w & F2(3), x & F2(2), x & F2(3), qs);
+    const uint32_t s0 = ksw[P4 + odd], s1 = ksw[P4 + 2 + odd];
+    const uint32_t h0 = hmul2u(lo32(qi), s0), h1 = hmul2u(hi32(qi), s1);
+    const uint64_t qs = pack_b64(h0, h1);
+    const uint32_t a00 = kcode(w, F2(0)), a01 = kcode(w, F2(1)), a02 = kcode(x, F2(0)), a03 = kcode(x, F2(1));
+    const uint32_t a10 = kcode(w, F2(2)), a11 = kcode(w, F2(3)), a12 = kcode(x, F2(2)), a13 = kcode(x, F2(3));
+    mma16816_b64(c0, a00, a01, a02, a03, qs);
+    mma16816_b64(c1, a10, a11, a12, a13, qs);
+#if KVMIX_Q2EXACT
+    // q*s has <= 19 significant bits (bf16 q) and h = RN16(q*s) keeps 11: the remainder
+    // q*s - h is an fp16 value, computed exactly by one fused HFMA2 (fp32 q: plus lo(q)*s,
+    // rounded once more at 2^-22 relative).  Its MMA makes the key products exact.
+    uint32_t r0 = hfma2u(lo32(qi), s0, hneg2u(h0)), r1 = hfma2u(hi32(qi), s1, hneg2u(h1));
+    if constexpr (LO) {
+      const uint64_t ql = qf.b2lo(i);
+      r0 = hfma2u(lo32(ql), s0, r0);
+      r1 = hfma2u(hi32(ql), s1, r1);
+    }
+    const uint64_t qr = pack_b64(r0, r1);
+#if KVMIX_Q2ACC
+    mma16816_b64(c0, a00, a01, a02, a03, qr);
+    mma16816_b64(c1, a10, a11, a12, a13, qr);
 #else
-    mma16816_b64(c0, w & F2(0), w & F2(1), x & F2(0), x & F2(1), qs);
-    mma16816_b64(c1, w & F2(2), w & F2(3), x & F2(2), x & F2(3), qs);
+    mma16816_b64(d0, a00, a01, a02, a03, qr);
+    mma16816_b64(d1, a10, a11, a12, a13, qr);
+#endif
 #endif
     mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qi);
     if constexpr (LO) mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qf.b2lo(i));
   }
   const float b0 = fmaf(cbE[0] + cbO[2], qscale, -st.m0), b1 = fmaf(cbE[1] + cbO[3], qscale, -st.m1);
-  const float f0 = P24 * qscale, f1 = P22 * qscale, f2 = P20 * qscale, f3 = P18 * qscale;
+  const float f0 = KF0 * qscale, f1 = KF1 * qscale, f2 = KF2 * qscale, f3 = KF3 * qscale;
   sv[0] = fmaf(c0[0] + d0[0], f0, b0);
   sv[1] = fmaf(c0[1] + d0[1], f0, b1);
   sv[2] = fmaf(c0[2] + d0[2], f1, b0);
@@ -494,7 +571,7 @@ __device__ __forceinline__ void int4_qk(const uint8_t* __restrict__ buf, int nv,
   using C = Cfg<D>;
   constexpr int S = C::SS, NG = C::NGRP;
   const int g = lane >> 2, q = lane & 3;
-  const float fs = P24 * qscale;  // every INT4 K product is at 2^-24 (high-nibble q is pre-divided by 16)
+  const float fs = KF4 * qscale;  // both nibbles' products at one scale (low-nibble q is pre-multiplied by 16)
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int sa = 16 * mt + rho(g), sb = sa + 8;
@@ -510,11 +587,13 @@ __device__ __forceinline__ void int4_qk(const uint8_t* __restrict__ buf, int nv,
       dj[j][0] = dj[j][1] = dj[j][2] = dj[j][3] = 0.f;
       const uint32_t wa = kwa[j], wb = kwb[j];
       const uint32_t xa = wa >> 8, xb = wb >> 8;
-      mma16816_b64(dj[j], wa & N4H, wb & N4H, wa & N4L, wb & N4L, qf.b4(2 * j));
-      mma16816_b64(dj[j], xa & N4L, xb & N4L, xa & N4H, xb & N4H, qf.b4(2 * j + 1));
+      const uint32_t e0 = kcode(wa, N4H), e1 = kcode(wb, N4H), e2 = kcode(wa, N4L), e3 = kcode(wb, N4L);
+      const uint32_t o0 = kcode(xa, N4L), o1 = kcode(xb, N4L), o2 = kcode(xa, N4H), o3 = kcode(xb, N4H);
+      mma16816_b64(dj[j], e0, e1, e2, e3, qf.b4(2 * j));
+      mma16816_b64(dj[j], o0, o1, o2, o3, qf.b4(2 * j + 1));
       if constexpr (LO) {
-        mma16816_b64(dj[j], wa & N4H, wb & N4H, wa & N4L, wb & N4L, qf.b4lo(2 * j));
-        mma16816_b64(dj[j], xa & N4L, xb & N4L, xa & N4H, xb & N4H, qf.b4lo(2 * j + 1));
+        mma16816_b64(dj[j], e0, e1, e2, e3, qf.b4lo(2 * j));
+        mma16816_b64(dj[j], o0, o1, o2, o3, qf.b4lo(2 * j + 1));
       }
     }
     // sum_j z_j Q_j: A row = token, k = 2q, 2q+1 -> groups 2q, 2q+1 (lanes with 2q >= NG give 0)
@@ -709,13 +788,25 @@ __device__ __forceinline__ void stage_q(const DecodeArgs& a, const Unit& u, floa
 }
 
 // Q fragments of one unit (see QFrag) written by one warp into the CTA's smem table, from
-// the unit's staged q rows (stage_q).
+// the unit's staged q rows (stage_q).  q enters pre-scaled by 2^-qexp (pool_bounds; 0 for
+// ordinary data) so that the fp16 operands cannot overflow; returns qscale * 2^qexp, the
+// factor that turns the tile accumulations back into log2-domain logits.
 template <int D, bool LO>
-__device__ __forceinline__ void build_qtab(const float* qraw, uint64_t* qtab, int lane) {
+__device__ __forceinline__ float build_qtab(const float* qraw, uint64_t* qtab, int lane, float qscale, int ek) {
   using C = Cfg<D>;
   using QF = QFrag<D, LO>;
   const int g = lane >> 2, q = lane & 3;
-  auto qv = [&](int c) { return qraw[g * C::QS + c]; };
+  float amax = 0.f;  // max |q| of the unit: lane (g, q) scans head g, channels [q D/4, (q+1) D/4)
+#pragma unroll
+  for (int c = 0; c < D / 4; c += 4) {
+    const float4 v = *reinterpret_cast<const float4*>(qraw + g * C::QS + q * (D / 4) + c);
+    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  const int qexp = min(30, max(0, ilog2f(fmaxf(amax, 1e-30f)) + ek - 13));
+  const float sc = __int_as_float((127 - qexp) << 23);  // 2^-qexp, exact
+  auto qv = [&](int c) { return qraw[g * C::QS + c] * sc; };
   auto lo = [](float x) { return x - __half2float(__float2half_rn(x)); };
   auto put = [&](int f, uint64_t v) { qtab[f * 32 + lane] = v; };
 #pragma unroll
@@ -732,13 +823,14 @@ __device__ __forceinline__ void build_qtab(const float* qraw, uint64_t* qtab, in
     float y[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) y[e] = qv(cb + e);
-    // high-nibble channels (cb+1, cb+5, cb+3, cb+7) enter at 2^-20: their q is divided by 16
-    constexpr float R16 = 0.0625f;
-    put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1] * R16, y[5] * R16), pack_h2(y[0], y[4])));
-    put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2], y[6]), pack_h2(y[3] * R16, y[7] * R16)));
+    // high-nibble channels (cb+1, cb+5, cb+3, cb+7) enter at 2^-20, low-nibble ones at 2^-24:
+    // the latter's q is multiplied by 16 (exact; small q stays a normal fp16 number)
+    constexpr float X16 = 16.f;
+    put(QF::NCH + 2 * j, pack_b64(pack_h2(y[1], y[5]), pack_h2(y[0] * X16, y[4] * X16)));
+    put(QF::NCH + 2 * j + 1, pack_b64(pack_h2(y[2] * X16, y[6] * X16), pack_h2(y[3], y[7])));
     if constexpr (LO) {
-      put(3 * QF::NCH + 2 + 2 * j, pack_b64(pack_h2(lo(y[1]) * R16, lo(y[5]) * R16), pack_h2(lo(y[0]), lo(y[4]))));
-      put(3 * QF::NCH + 2 + 2 * j + 1, pack_b64(pack_h2(lo(y[2]), lo(y[6])), pack_h2(lo(y[3]) * R16, lo(y[7]) * R16)));
+      put(3 * QF::NCH + 2 + 2 * j, pack_b64(pack_h2(lo(y[1]), lo(y[5])), pack_h2(lo(y[0]) * X16, lo(y[4]) * X16)));
+      put(3 * QF::NCH + 2 + 2 * j + 1, pack_b64(pack_h2(lo(y[2]) * X16, lo(y[6]) * X16), pack_h2(lo(y[3]), lo(y[7]))));
     }
     float part = ((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]));
     part += __shfl_xor_sync(0xffffffffu, part, 1);
@@ -748,25 +840,30 @@ __device__ __forceinline__ void build_qtab(const float* qraw, uint64_t* qtab, in
   }
   put(2 * QF::NCH, pack_b64(pack_h2(qa, qb), 0u));
   put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
+  return qscale * __int_as_float((127 + qexp) << 23);
 }
 
 // K4 fused decode append, cold path (out of line): channel group j of the request's newest
 // token -> the staged slot record srec and its place in the pool.
 template <int D>
-__device__ __noinline__ void append_group(const DecodeArgs& a, const Unit& u, uint8_t* srec, int j) {
+__device__ __noinline__ float append_group(const DecodeArgs& a, const Unit& u, uint8_t* srec, int j) {
   using C = Cfg<D>;
   const int64_t slot = a.int4_ids[u.i40 + u.n4 - 1];
   uint8_t* grec = a.int4_pool_w + ((a.layer * a.n_kv + u.kvh) * a.pool_int4 + slot) * (int64_t)C::SS;
   const int64_t off = ((int64_t)u.b * a.n_kv + u.kvh) * D + 32 * j;
+  int32_t* err = a.pool_status ? a.pool_status + KVMIX_POOL_STATUS_ERR : nullptr;
+  float vs;
   if (a.app_dtype == KVMIX_BF16)
-    encode_int4_group<D, __nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(a.app_k) + off,
-                                        reinterpret_cast<const __nv_bfloat16*>(a.app_v) + off, srec, grec, j, nullptr);
+    vs = encode_int4_group<D, __nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(a.app_k) + off,
+                                             reinterpret_cast<const __nv_bfloat16*>(a.app_v) + off, srec, grec, j, err);
   else if (a.app_dtype == KVMIX_F16)
-    encode_int4_group<D, __half>(reinterpret_cast<const __half*>(a.app_k) + off,
-                                 reinterpret_cast<const __half*>(a.app_v) + off, srec, grec, j, nullptr);
+    vs = encode_int4_group<D, __half>(reinterpret_cast<const __half*>(a.app_k) + off,
+                                      reinterpret_cast<const __half*>(a.app_v) + off, srec, grec, j, err);
   else
-    encode_int4_group<D, float>(reinterpret_cast<const float*>(a.app_k) + off,
-                                reinterpret_cast<const float*>(a.app_v) + off, srec, grec, j, nullptr);
+    vs = encode_int4_group<D, float>(reinterpret_cast<const float*>(a.app_k) + off,
+                                     reinterpret_cast<const float*>(a.app_v) + off, srec, grec, j, err);
+  if (a.pool_status) atomicMax(a.pool_status + KVMIX_POOL_STATUS_VSCALE, __float_as_int(vs));
+  return vs;
 }
 
 // Issue this warp's first STAGES tiles of piece u into its ring, starting at `stage`.
@@ -818,6 +915,7 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   const int g = lane >> 2, q = lane & 3;
   uint8_t* ring = smem + warp * STAGES * C::BUF;
   __shared__ int sm_flag;
+  __shared__ float sm_qscale;
 
   if (lane == 0) {
 #pragma unroll
@@ -830,6 +928,11 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   uint32_t phase = 0;
   bool waited = false;  // q, out, partials and counters are touched only after pdl_wait()
 
+  if (a.flags & KVMIX_DECODE_POOL_WRITTEN) {  // the previous kernel wrote the pool: no early KV copies
+    pdl_wait();
+    waited = true;
+  }
+  Bounds bnd{RESCALE_SLACK, 5};
   const int piece_end = a.cta_ptr[blockIdx.x + 1];
   bool primed = false;  // the piece's first tiles were issued while the previous piece merged
 #ifdef KVMIX_CTA_TIMES
@@ -876,21 +979,26 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
     if (threadIdx.x == 0 && blockIdx.x < 4096) g_cta_times[blockIdx.x][1] = gtimer();
 #endif
   }
+  if (piece == a.cta_ptr[blockIdx.x]) bnd = pool_bounds(a.pool_status);  // written by earlier kernels
   uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + NW * STAGES * C::BUF);
   float* qraw = reinterpret_cast<float*>(smem + NW * STAGES * C::BUF + C::QTAB + (C::MERGE_IN_RING ? 0 : C::MERGE));
   stage_q<D>(a, u, qraw);
   __syncthreads();
-  if (warp == 0) build_qtab<D, LO>(qraw, qtab, lane);
+  if (warp == 0) {
+    const float qs = build_qtab<D, LO>(qraw, qtab, lane, a.qscale, bnd.ek);
+    if (lane == 0) sm_qscale = qs;
+  }
   __syncthreads();
   KVMIX_STAMP(1)
   const QFrag<D, LO> qf{qtab + lane};
+  const float qscale = sm_qscale;
 
   Acc<D> acc;
 #pragma unroll
   for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
   acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
   acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
-  Softmax st{0.f, 0.f, false};
+  Softmax st{0.f, 0.f, false, bnd.slack};
 
   for (int k = 0; k < nmine; ++k) {
     const int t = u.tlo + warp + k * NW;
@@ -904,18 +1012,23 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
 #endif
     if (MEMORY) mbar_wait(&bars[warp][stage], phase);
     if (APPEND && u.n4 > 0 && t == u.npg + (u.n4 - 1) / 32) {
-      // K4 fused: quantize the newest token over the stale copy the TMA brought in
-      if (lane < C::NGRP) append_group<D>(a, u, ring + stage * C::BUF + ((u.n4 - 1) % 32) * C::SS, lane);
+      // K4 fused: quantize the newest token over the stale copy the TMA brought in; a V
+      // scale beyond this launch's bound switches the warp to exact-max softmax (p <= 1)
+      float vs = 0.f;
+      if (lane < C::NGRP) vs = append_group<D>(a, u, ring + stage * C::BUF + ((u.n4 - 1) % 32) * C::SS, lane);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) vs = fmaxf(vs, __shfl_xor_sync(0xffffffffu, vs, off));
+      if (15 - ilog2f(fmaxf(vs, 1.f)) < (int)st.slack) st.slack = 0.f;
       __syncwarp();
     }
     if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
     } else if (t < u.npg) {
-      int2_tile<D, LO>(buf, qf, a.qscale, lane, st, acc);
+      int2_tile<D, LO>(buf, qf, qscale, lane, st, acc);
     } else {
       const int nv = min(32, u.n4 - 32 * (t - u.npg));
-      if (nv == 32) int4_tile<D, true, LO>(buf, 32, qf, a.qscale, lane, st, acc);
-      else int4_tile<D, false, LO>(buf, nv, qf, a.qscale, lane, st, acc);
+      if (nv == 32) int4_tile<D, true, LO>(buf, 32, qf, qscale, lane, st, acc);
+      else int4_tile<D, false, LO>(buf, nv, qf, qscale, lane, st, acc);
     }
     __syncwarp();
     if (MEMORY && k + STAGES < nmine) {
@@ -964,8 +1077,9 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
 #endif
 }
 
+#ifdef KVMIX_MEASURE_VARIANTS
 // ====================================================================================
-// Variant 4: warp-specialised tensor-core kernel.  A CTA holds NPAIR pairs of warps; in
+// Variant 4 (measurement builds only, -DKVMIX_MEASURE_VARIANTS): warp-specialised tensor-core kernel.  A CTA holds NPAIR pairs of warps; in
 // pair p, warp p (QK) issues the TMA copies of the pair's tiles and computes the logits
 // S = QK^T (dequantised in registers), handing them (32 B per lane) to warp p + NPAIR (PV)
 // through the tile's own ring slot; the PV warp runs the online softmax and owns the
@@ -997,6 +1111,7 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
   __shared__ __align__(8) uint64_t full[NPAIR][WSTAGES], pready[NPAIR][WSTAGES], empty[NPAIR][WSTAGES];
   __shared__ float sm_m[NPAIR * 8], sm_l[NPAIR * 8];
   __shared__ int sm_flag;
+  __shared__ float sm_qscale;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const bool is_qk = warp < NPAIR;
@@ -1022,10 +1137,15 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
     const int nmine = ntiles > pair ? (ntiles - pair + NPAIR - 1) / NPAIR : 0;
     auto tile_of = [&](int k) { return u.tlo + pair + k * NPAIR; };
     float* qraw = reinterpret_cast<float*>(smem + W::RING + (D / 8 + 2) * 32 * 8 * 2);
+    const Bounds bnd = pool_bounds(a.pool_status);
     stage_q<D>(a, u, qraw);
     __syncthreads();
-    if (warp == 0) build_qtab<D, LO>(qraw, qtab, lane);
+    if (warp == 0) {
+      const float qs = build_qtab<D, LO>(qraw, qtab, lane, a.qscale, bnd.ek);
+      if (lane == 0) sm_qscale = qs;
+    }
     __syncthreads();
+    const float qscale = sm_qscale;
 
     if (is_qk) {
       const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
@@ -1040,7 +1160,7 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
       for (int k = 0; k < WSTAGES - 2 && k < nmine; ++k) do_issue(k, meta_of(k));
       int meta_next = meta_of(WSTAGES - 2);  // index loads run one tile ahead of their copies
       const QFrag<D, LO> qf{qtab + lane};
-      const Softmax s0{0.f, 0.f, false};  // the QK warp emits unshifted logits; the PV warp owns the max
+      const Softmax s0{0.f, 0.f, false, bnd.slack};  // the QK warp emits unshifted logits; the PV warp owns the max
       for (int k = 0; k < nmine; ++k) {
         const uint32_t gk = kg + k;
         const int s = gk % WSTAGES;
@@ -1049,11 +1169,11 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
         const int t = tile_of(k);
         float sv[8];
         if (t < u.npg) {
-          int2_qk<D, LO>(buf, qf, a.qscale, lane, s0, sv);
+          int2_qk<D, LO>(buf, qf, qscale, lane, s0, sv);
         } else {
           const int nv = min(32, u.n4 - 32 * (t - u.npg));
-          if (nv == 32) int4_qk<D, true, LO>(buf, 32, qf, a.qscale, lane, s0, sv);
-          else int4_qk<D, false, LO>(buf, nv, qf, a.qscale, lane, s0, sv);
+          if (nv == 32) int4_qk<D, true, LO>(buf, 32, qf, qscale, lane, s0, sv);
+          else int4_qk<D, false, LO>(buf, nv, qf, qscale, lane, s0, sv);
         }
         float4* sa = reinterpret_cast<float4*>(buf + C::BUF) + 2 * lane;
         sa[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
@@ -1075,7 +1195,7 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
       for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
       acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
       acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
-      Softmax st{0.f, 0.f, false};
+      Softmax st{0.f, 0.f, false, bnd.slack};
       for (int k = 0; k < nmine; ++k) {
         const uint32_t gk = kg + k;
         const int s = gk % WSTAGES;
@@ -1119,6 +1239,8 @@ __global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kerne
     __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
   }
 }
+
+#endif  // KVMIX_MEASURE_VARIANTS
 
 // ====================================================================================
 // Variant 1: simple CUDA-core kernel (fp32 dequant straight from HBM).  Slow; kept as
@@ -1244,13 +1366,15 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
       }
       if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_mma_kernel<D, true, true, true>, a, n_work, Cfg<D>::SMEM, s);
       return launch_kernel(decode_mma_kernel<D, true, true, false>, a, n_work, Cfg<D>::SMEM, s);
+    case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, NW * 8 * D * (int)sizeof(float), s);
+#ifdef KVMIX_MEASURE_VARIANTS
     case 4:
       if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_ws_kernel<D, true>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
       return launch_kernel(decode_ws_kernel<D, false>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
-    case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, NW * 8 * D * (int)sizeof(float), s);
     case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
     case 3: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
-    default: return fail(KVMIX_EINVAL, "bad variant");
+#endif
+    default: return fail(KVMIX_EINVAL, "variant not built (2-4 need -DKVMIX_MEASURE_VARIANTS)");
   }
 }
 
@@ -1291,7 +1415,8 @@ static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t 
                              const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
                              const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
                              float* partials, int32_t* counters, float scale, int32_t variant, const void* k_new,
-                             const void* v_new, int32_t kv_dtype, uint8_t* int4_pool_w, void* stream) {
+                             const void* v_new, int32_t kv_dtype, uint8_t* int4_pool_w, int32_t* pool_status,
+                             int32_t flags, void* stream) {
   if (n_kv <= 0 || n_q % n_kv) return fail(KVMIX_EINVAL, "n_heads not a multiple of the pool's n_kv_heads");
   const int64_t gq = n_q / n_kv;
   if (gq > 8) return fail(KVMIX_EINVAL, "GQA group > 8 not supported");
@@ -1326,6 +1451,8 @@ static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t 
   a.app_v = v_new;
   a.app_dtype = kv_dtype;
   a.int4_pool_w = int4_pool_w;
+  a.pool_status = pool_status;
+  a.flags = flags;
   if (k_new != nullptr) {
     if (variant != 0) return fail(KVMIX_EINVAL, "the fused decode append runs in the tensor-core kernel (variant 0)");
     if (!v_new || !int4_pool_w || kv_dtype < 0 || kv_dtype > 2) return fail(KVMIX_EINVAL, "bad append arguments");
@@ -1345,10 +1472,10 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
                                   int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
                                   const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
                                   const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
-                                  float scale, int32_t variant, void* stream) {
+                                  float scale, int32_t variant, int32_t* pool_status, int32_t flags, void* stream) {
   return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
                            batch, page_indptr, page_ids, int4_indptr, int4_ids, work, cta_ptr, n_cta, partials,
-                           counters, scale, variant, nullptr, nullptr, 0, nullptr, stream);
+                           counters, scale, variant, nullptr, nullptr, 0, nullptr, pool_status, flags, stream);
 }
 
 extern "C" int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
@@ -1358,9 +1485,9 @@ extern "C" int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* o
                                          const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
                                          const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
                                          float scale, const void* k_new, const void* v_new, int32_t kv_dtype,
-                                         void* stream) {
+                                         int32_t* pool_status, int32_t flags, void* stream) {
   if (!k_new || !v_new) return fail(KVMIX_EINVAL, "k_new / v_new are required");
   return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
                            batch, page_indptr, page_ids, int4_indptr, int4_ids, work, cta_ptr, n_cta, partials,
-                           counters, scale, 0, k_new, v_new, kv_dtype, int4_pool, stream);
+                           counters, scale, 0, k_new, v_new, kv_dtype, int4_pool, pool_status, flags, stream);
 }

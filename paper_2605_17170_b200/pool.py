@@ -139,7 +139,13 @@ class MixedPrecisionPool:
                                          device=self.device)
             self.int4_pool = torch.zeros(max(1, L * H * self.n_int4 * self.slot_stride), dtype=torch.uint8,
                                          device=self.device)
-            self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
+            # pool status words (kvmix_b200.h KVMIX_POOL_STATUS_*): error bits, largest stored
+            # key-page / V scales (the decode kernel's fp16 operand bounds)
+            self.status = torch.zeros(_lib.POOL_STATUS_WORDS, dtype=torch.int32, device=self.device)
+        # the last pool kernel launched was a writer (True: all layers; int: that layer only):
+        # a decode of those layers must not prefetch KV ahead of it (programmatic dependent
+        # launch); False once a decode has run after it
+        self._written = False
 
     # -- address helpers -------------------------------------------------------------
     def is_int2(self, address: SlotAddress) -> bool:
@@ -288,9 +294,15 @@ class MixedPrecisionPool:
         return torch.as_tensor(np.asarray(x, dtype=np.float32), device=self.device).contiguous()
 
     def _check_err(self, what: str) -> None:
-        if int(self._err.item()) & 1:
-            self._err.zero_()
+        err = self.status[_lib.POOL_STATUS_ERR]
+        if int(err.item()) & 1:
+            err.zero_()
             raise ValidationError(f"{what} must be finite")
+
+    def operand_bounds(self) -> tuple[float, float]:
+        """(largest INT2 key-page scale, largest V scale) written so far (pool status words)."""
+        w = self.status.cpu().numpy().view(np.float32)
+        return float(w[_lib.POOL_STATUS_KSCALE]), float(w[_lib.POOL_STATUS_VSCALE])
 
     def write_page(self, page_start: int, keys, values, layer: int, head: int) -> None:
         """pool.py:201-215: one full INT2 page (all G tokens) for one (layer, head)."""
@@ -311,7 +323,8 @@ class MixedPrecisionPool:
         _lib.check(lib.kvmix_write_prefill(
             k.data_ptr(), v.data_ptr(), _lib.dtype_code(k), 1, g, 1, cfg.head_dim, toks.data_ptr(),
             pid.data_ptr(), 1, None, None, 0, self.int2_pool.data_ptr() + off2, self.n_pages,
-            self.int4_pool.data_ptr(), self.n_int4, self._err.data_ptr(), _lib.stream()))
+            self.int4_pool.data_ptr(), self.n_int4, self.status.data_ptr(), _lib.stream()))
+        self._written = True
         self._check_err("keys/values")
         self._page_written[layer, head, page_start // g] = True
 
@@ -328,7 +341,8 @@ class MixedPrecisionPool:
         ids = torch.tensor([slot - self.config.offset], dtype=torch.int32, device=self.device)
         _lib.check(lib.kvmix_append_int4(kk.data_ptr(), vv.data_ptr(), _lib.dtype_code(kk), 1, 1, 0, 1, 1,
                                          self.config.head_dim, ids.data_ptr(), self.int4_pool.data_ptr() + off4,
-                                         self.n_int4, self._err.data_ptr(), _lib.stream()))
+                                         self.n_int4, self.status.data_ptr(), _lib.stream()))
+        self._written = True
         self._check_err("values")
         self._int4_written[layer, head, slot - self.config.offset] = True
 
@@ -368,9 +382,12 @@ class MixedPrecisionPool:
             k.data_ptr(), v.data_ptr(), _lib.dtype_code(k), cfg.n_layers, n, cfg.n_kv_heads, cfg.head_dim,
             pt.data_ptr(), pi.data_ptr(), pi.numel(), it.data_ptr(), ii.data_ptr(), it.numel(),
             self.int2_pool.data_ptr(), self.n_pages, self.int4_pool.data_ptr(), self.n_int4,
-            self._err.data_ptr(), _lib.stream()))
+            self.status.data_ptr(), _lib.stream()))
+        self._written = True
         if check_finite:
             self._check_err("keys/values")
+        else:  # the caller opted out: a non-finite input must not fail a later, finite write
+            self.status[_lib.POOL_STATUS_ERR].zero_()
         self._page_written[:, :, page_ids] = True
         self._int4_written[:, :, s[t4] - cfg.offset] = True
 
@@ -443,8 +460,9 @@ class MixedPrecisionPool:
         ids = torch.tensor([slot - cfg.offset], dtype=torch.int32, device=self.device)
         _lib.check(lib.kvmix_append_int4(kk.data_ptr(), vv.data_ptr(), _lib.dtype_code(kk), 1, cfg.n_layers, 0,
                                          cfg.n_layers, cfg.n_kv_heads, cfg.head_dim, ids.data_ptr(),
-                                         self.int4_pool.data_ptr(), self.n_int4, self._err.data_ptr(),
+                                         self.int4_pool.data_ptr(), self.n_int4, self.status.data_ptr(),
                                          _lib.stream()))
+        self._written = True
         self._check_err("decode k/v")
         self._int4_written[:, :, slot - cfg.offset] = True
         table._set_slots(np.append(table.slots, slot))
@@ -487,7 +505,9 @@ class MixedPrecisionPool:
             lin, l0 = 1, layer
         _lib.check(lib.kvmix_append_int4(k.data_ptr(), v.data_ptr(), _lib.dtype_code(k), B, lin, l0,
                                          cfg.n_layers, cfg.n_kv_heads, cfg.head_dim, ids.data_ptr(),
-                                         self.int4_pool.data_ptr(), self.n_int4, None, _lib.stream()))
+                                         self.int4_pool.data_ptr(), self.n_int4, self.status.data_ptr(),
+                                         _lib.stream()))
+        self._written = True
         self._int4_written[l0:l0 + lin, :, slots - cfg.offset] = True
         return slots
 

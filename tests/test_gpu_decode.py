@@ -75,7 +75,14 @@ def test_random_instances_vs_oracle(cuda):
 
 def test_warp_specialised_variant(cuda):
     """Variant 4 (QK warps hand logits to PV/softmax warps) gives the same results as the
-    default kernel (same math, same fp16 roundings; only the order of fp32 sums differs)."""
+    default kernel (same math, same fp16 roundings; only the order of fp32 sums differs).
+    Measurement builds only (-DKVMIX_MEASURE_VARIANTS); the product library omits it."""
+    pool, t, *_ = build(1, 64, 1, 128, 0.5)
+    b = kv.DecodeBatch(pool, ["req"], n_q_heads=8)
+    try:
+        kv.flash_decode_batched(torch.zeros(1, 8, 128, device=cuda), b, 0, variant=4)
+    except kv.ValidationError:
+        pytest.skip("variant 4 not built (measurement builds only)")
     rng = np.random.default_rng(7)
     for i in range(40):
         d = int(rng.choice([32, 64, 128]))
@@ -189,8 +196,7 @@ def test_batched_mixed_lengths_and_dtypes(cuda):
             kv.flash_decode_batched(qq, batch, layer, out=out)
             for r in range(len(lens)):
                 ref = oatt.flash_decode_pool(qq[r].float().cpu().numpy(), op, f"r{r}", layer)
-                atol = ATOL + (4e-3 if od == torch.bfloat16 else 0.0)  # bf16 output rounding
-                ok, err = close(out[r].float().cpu().numpy(), ref, atol=atol)
+                ok, err = close(out[r].float().cpu().numpy(), ref)
                 assert ok, (layer, qd, od, r, err)
 
 
