@@ -160,6 +160,8 @@ int kvmix_route_tokens(const int8_t* bits, int64_t n, int32_t page_size, const i
  *   q [batch][n_q_heads][d] (q_dtype), out [batch][n_q_heads][d] (out_dtype)
  *   page_indptr[batch+1], page_ids[]: INT2 page list of each partitioned table (table order)
  *   int4_indptr[batch+1], int4_ids[]: INT4 indices of each table's suffix (table order)
+ *   int4_count: NULL for CSR lists; else request b's INT4 list is int4_ids[int4_indptr[b] ..
+ *     int4_indptr[b] + int4_count[b]) (the padded lists kept by kvmix_decode_tables)
  *   The tiles of a unit (request b, kv head h; unit = b*Hkv + h) are its INT2 pages then
  *   ceil(n_int4/32) INT4 tiles of 32 slots, so every tile is bitwidth-homogeneous.
  *   work [n_pieces][8] = {unit, tile_lo, tile_hi, slot, part0, nparts, 0, 0}: a piece is a
@@ -185,9 +187,9 @@ int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dt
                        const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
                        int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
                        const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
-                       const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
-                       float* partials, int32_t* counters, float scale, int32_t variant, int32_t* pool_status,
-                       int32_t flags, void* stream);
+                       const int32_t* int4_ids, const int32_t* int4_count, const int32_t* work,
+                       const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters, float scale,
+                       int32_t variant, int32_t* pool_status, int32_t flags, void* stream);
 
 /* K4 fused decode append (pool.py:284-306 append_decode_token data half + attention.py:175
  * flash_decode, one launch): the same as kvmix_flash_decode (variant 0) for one layer, where
@@ -199,9 +201,23 @@ int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* out, int32_t
                               uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4, int64_t layer,
                               int64_t n_kv_heads, int64_t head_dim, int64_t n_q_heads, int64_t batch,
                               const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
-                              const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
-                              float* partials, int32_t* counters, float scale, const void* k_new, const void* v_new,
-                              int32_t kv_dtype, int32_t* pool_status, int32_t flags, void* stream);
+                              const int32_t* int4_ids, const int32_t* int4_count, const int32_t* work,
+                              const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters, float scale,
+                              const void* k_new, const void* v_new, int32_t kv_dtype, int32_t* pool_status,
+                              int32_t flags, void* stream);
+
+/* K7 decode-step tables (pool.py:284-306 append_decode_token, the device half): append
+ * new_slots[b] (INT4 index = slot - offset; NULL = no append) to request b's padded INT4
+ * list int4_ids[b * cap + int4_count[b]] and bump int4_count[b] (err bit 2 when full), then
+ * rebuild the decode kernel's stream-K plan for n_pages[b] INT2 pages and int4_count[b]
+ * INT4 slots per request: work [n_cta + batch * n_kv][8] (capacity), cta_ptr [n_cta + 1],
+ * n_parts [1] (partial slots used, <= n_cta + batch * n_kv), scratch int32 [2 * batch * n_kv].
+ * Use with kvmix_flash_decode(_append)(int4_indptr[b] = b * cap, int4_count, ...). */
+int64_t kvmix_decode_tables_smem(int64_t batch, int64_t n_cta);
+int kvmix_decode_tables(const int32_t* new_slots, int64_t batch, int64_t n_kv, const int32_t* n_pages,
+                        int32_t* int4_count, int32_t* int4_ids, int64_t cap, int64_t head_dim, float int4_weight,
+                        int64_t n_cta, int32_t* work, int32_t* cta_ptr, int32_t* n_parts, int32_t* scratch,
+                        int32_t* err, void* stream);
 
 /* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
  * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */

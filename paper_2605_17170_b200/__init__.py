@@ -17,6 +17,7 @@ from .attention import (
     merge_partials,
 )
 from . import calib  # noqa: F401  (calibration replay on the GPU)
+from .decode_step import DecodeStep
 from .errors import CapacityError, InfeasibleBudgetError, KvmixError, TemplateStructureError, ValidationError
 from .plan import plan_stream
 from .pool import (

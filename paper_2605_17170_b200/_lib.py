@@ -52,9 +52,12 @@ _SIGS = {
     "kvmix_gather_dequant_typed": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P],
                                    ctypes.c_int),
     "kvmix_flash_decode": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
-                            _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
+                            _P, _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
     "kvmix_flash_decode_append": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P,
-                                   _P, _P, _P, _I64, _P, _P, _F, _P, _P, _I32, _P, _I32, _P], ctypes.c_int),
+                                   _P, _P, _P, _P, _I64, _P, _P, _F, _P, _P, _I32, _P, _I32, _P], ctypes.c_int),
+    "kvmix_decode_tables_smem": ([_I64, _I64], _I64),
+    "kvmix_decode_tables": ([_P, _I64, _I64, _P, _P, _P, _I64, _I64, _F, _I64, _P, _P, _P, _P, _P, _P],
+                            ctypes.c_int),
     "kvmix_merge_partials": ([_P, _P, _P, _I64, _I64, _P, _P], ctypes.c_int),
     "kvmix_route_scratch_elems": ([_I64], _I64),
     "kvmix_count_int2": ([_P, _I64, _P, _P, _P], ctypes.c_int),

@@ -179,7 +179,7 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
             q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
             pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,
             batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
-            t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
+            t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), None, batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
             batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), k_new.data_ptr(),
             v_new.data_ptr(), _lib.dtype_code(k_new), pool.status.data_ptr(), flags, _lib.stream()))
         pool._int4_written[layer, :, batch.last_int4 - cfg.offset] = True
@@ -189,7 +189,7 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
         q.data_ptr(), _lib.dtype_code(q), out.data_ptr(), _lib.dtype_code(out), pool.int2_pool.data_ptr(),
         pool.int4_pool.data_ptr(), pool.n_pages, pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim,
         batch.n_q_heads, batch.batch, t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(),
-        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
+        t["int4_indptr"].data_ptr(), t["int4_ids"].data_ptr(), None, batch.work.data_ptr(), batch.cta_ptr.data_ptr(),
         batch.n_cta, batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), int(variant),
         pool.status.data_ptr(), flags, _lib.stream()))
     pool._written = False

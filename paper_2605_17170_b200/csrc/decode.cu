@@ -92,6 +92,7 @@ struct DecodeArgs {
   const int32_t* page_ids;
   const int32_t* int4_indptr;
   const int32_t* int4_ids;
+  const int32_t* int4_count;  // NULL: CSR (count = indptr[b+1] - indptr[b]); else padded lists (K7)
   const int32_t* work;     // pieces [n][8]: unit, tile_lo, tile_hi, slot (-1: whole unit), part0, nparts
   const int32_t* cta_ptr;  // [grid + 1]: pieces of CTA i are cta_ptr[i] .. cta_ptr[i+1]
   float* part;             // split partials [n_parts][8][D + 4] (acc[D], m, l, pad; log2 domain)
@@ -138,7 +139,7 @@ __device__ __forceinline__ Unit load_unit(const DecodeArgs& a, int piece) {
   u.pg0 = a.page_indptr[u.b];
   u.npg = a.page_indptr[u.b + 1] - (int)u.pg0;
   u.i40 = a.int4_indptr[u.b];
-  u.n4 = a.int4_indptr[u.b + 1] - (int)u.i40;
+  u.n4 = a.int4_count ? a.int4_count[u.b] : a.int4_indptr[u.b + 1] - (int)u.i40;
   return u;
 }
 
@@ -1413,7 +1414,8 @@ static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t 
                              const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4,
                              int64_t layer, int64_t n_kv, int64_t d, int64_t n_q, int64_t batch,
                              const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
-                             const int32_t* int4_ids, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
+                             const int32_t* int4_ids, const int32_t* int4_count, const int32_t* work,
+                             const int32_t* cta_ptr, int64_t n_cta,
                              float* partials, int32_t* counters, float scale, int32_t variant, const void* k_new,
                              const void* v_new, int32_t kv_dtype, uint8_t* int4_pool_w, int32_t* pool_status,
                              int32_t flags, void* stream) {
@@ -1442,6 +1444,7 @@ static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t 
   a.page_ids = page_ids;
   a.int4_indptr = int4_indptr;
   a.int4_ids = int4_ids;
+  a.int4_count = int4_count;
   a.work = work;
   a.cta_ptr = cta_ptr;
   a.part = partials;
@@ -1470,11 +1473,12 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
                                   const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
                                   int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
                                   int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
-                                  const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
-                                  const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
-                                  float scale, int32_t variant, int32_t* pool_status, int32_t flags, void* stream) {
+                                  const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* int4_count,
+                                  const int32_t* work, const int32_t* cta_ptr, int64_t n_cta, float* partials,
+                                  int32_t* counters, float scale, int32_t variant, int32_t* pool_status, int32_t flags,
+                                  void* stream) {
   return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
-                           batch, page_indptr, page_ids, int4_indptr, int4_ids, work, cta_ptr, n_cta, partials,
+                           batch, page_indptr, page_ids, int4_indptr, int4_ids, int4_count, work, cta_ptr, n_cta, partials,
                            counters, scale, variant, nullptr, nullptr, 0, nullptr, pool_status, flags, stream);
 }
 
@@ -1482,12 +1486,12 @@ extern "C" int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* o
                                          uint8_t* int2_pool, uint8_t* int4_pool, int64_t pool_pages,
                                          int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
                                          int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
-                                         const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* work,
-                                         const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters,
-                                         float scale, const void* k_new, const void* v_new, int32_t kv_dtype,
-                                         int32_t* pool_status, int32_t flags, void* stream) {
+                                         const int32_t* int4_indptr, const int32_t* int4_ids, const int32_t* int4_count,
+                                         const int32_t* work, const int32_t* cta_ptr, int64_t n_cta, float* partials,
+                                         int32_t* counters, float scale, const void* k_new, const void* v_new,
+                                         int32_t kv_dtype, int32_t* pool_status, int32_t flags, void* stream) {
   if (!k_new || !v_new) return fail(KVMIX_EINVAL, "k_new / v_new are required");
   return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
-                           batch, page_indptr, page_ids, int4_indptr, int4_ids, work, cta_ptr, n_cta, partials,
+                           batch, page_indptr, page_ids, int4_indptr, int4_ids, int4_count, work, cta_ptr, n_cta, partials,
                            counters, scale, 0, k_new, v_new, kv_dtype, int4_pool, pool_status, flags, stream);
 }

@@ -43,11 +43,32 @@ class PageTable:
 
     def __init__(self, request_id: str, slots=None, partitioned: bool = False):
         self.request_id = request_id
-        self.slots = np.asarray(slots if slots is not None else [], dtype=np.int64)
+        self.slots = slots if slots is not None else []
         self.partitioned = partitioned
         self._entries_cache = None
         # (page_tokens, page_ids, int4_tokens, int4_ids) device tensors left by alloc_device
         # (K6) for write_prefill; dropped whenever the slots change
+        self._dev_index = None
+
+    @property
+    def slots(self) -> np.ndarray:
+        return self._buf[: self._n]
+
+    @slots.setter
+    def slots(self, value) -> None:
+        self._buf = np.array(value, dtype=np.int64)
+        self._n = int(self._buf.size)
+        self._entries_cache = None
+
+    def _append(self, slot: int) -> None:
+        """Amortised O(1) append of a decode slot (pool.py:305 entries.append)."""
+        if self._n == self._buf.size:
+            grown = np.empty(max(64, 2 * self._n), dtype=np.int64)
+            grown[: self._n] = self._buf[: self._n]
+            self._buf = grown
+        self._buf[self._n] = slot
+        self._n += 1
+        self._entries_cache = None
         self._dev_index = None
 
     @property
@@ -58,12 +79,10 @@ class PageTable:
 
     @entries.setter
     def entries(self, value) -> None:
-        self.slots = np.asarray([a.index for a in value], dtype=np.int64)
-        self._entries_cache = None
+        self.slots = [a.index for a in value]
 
     def _set_slots(self, slots) -> None:
-        self.slots = np.asarray(slots, dtype=np.int64)
-        self._entries_cache = None
+        self.slots = slots
         self._dev_index = None
 
     def __len__(self) -> int:
@@ -465,7 +484,7 @@ class MixedPrecisionPool:
         self._written = True
         self._check_err("decode k/v")
         self._int4_written[:, :, slot - cfg.offset] = True
-        table._set_slots(np.append(table.slots, slot))
+        table._append(slot)
         return SlotAddress(slot)
 
     def reserve_decode_slots(self, request_ids) -> np.ndarray:
@@ -485,8 +504,7 @@ class MixedPrecisionPool:
             s = self._free_int4.pop()
             slots[i] = s
             self._owner[s] = self._rid_index[rid]
-            t = self._tables[rid]
-            t._set_slots(np.append(t.slots, s))
+            self._tables[rid]._append(s)
         return slots
 
     def append_decode_tokens(self, request_ids, k: torch.Tensor, v: torch.Tensor, layer: int | None = None,

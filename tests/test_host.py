@@ -72,7 +72,7 @@ def test_abi_validation_without_gpu():
     with pytest.raises(kv.ValidationError):
         _lib.check(rc)
     rc = _lib.lib.kvmix_flash_decode(None, 0, None, 0, None, None, 1, 1, 0, 3, 128, 8, 1, None, None, None, None,
-                                     None, None, 3, None, None, 1.0, 0, None, 0, None)
+                                     None, None, None, 3, None, None, 1.0, 0, None, 0, None)
     with pytest.raises(kv.ValidationError, match="multiple"):
         _lib.check(rc)
 
