@@ -14,7 +14,8 @@ import torch
 
 from .errors import CapacityError, KvmixError, ValidationError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkvmix_b200.so")
+# KVMIX_LIB: an alternative build of the same library (measurement variants, tools/ab_variants.py)
+LIB_PATH = os.environ.get("KVMIX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkvmix_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -62,12 +62,11 @@ def adopt_table(pool, request_id: str, slots: np.ndarray, partitioned: bool = Fa
     slots = np.asarray(slots, dtype=np.int64)
     pages = np.unique(slots[slots < cfg.offset] // g * g)
     int4 = slots[slots >= cfg.offset]
-    free_pages = set(pool._free_pages)
-    free_int4 = set(pool._free_int4)
-    if not set(pages.tolist()) <= free_pages or not set(int4.tolist()) <= free_int4:
+    taken_pages, taken_int4 = set(pages.tolist()), set(int4.tolist())  # built once: O(|free| + |table|)
+    if not taken_pages <= set(pool._free_pages) or not taken_int4 <= set(pool._free_int4):
         raise ValidationError("adopted table uses slots that are not free on this rank")
-    pool._free_pages = [p for p in pool._free_pages if p not in set(pages.tolist())]
-    pool._free_int4 = [s for s in pool._free_int4 if s not in set(int4.tolist())]
+    pool._free_pages = [p for p in pool._free_pages if p not in taken_pages]
+    pool._free_int4 = [s for s in pool._free_int4 if s not in taken_int4]
     rix = pool._next_rid
     pool._next_rid += 1
     pool._rid_index[request_id] = rix
