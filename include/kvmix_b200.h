@@ -74,6 +74,10 @@ int kvmix_decode_token_blocks(const uint8_t* blocks, int64_t n, int64_t head_dim
  * codes written at the same positions, scale/zero per group (fp32 holding the fp16 value). */
 int kvmix_quantize_groups(const float* x, const int64_t* offsets, int64_t n_groups, int32_t bitwidth,
                           uint8_t* codes, float* scale, float* zero, int32_t* err_flag, void* stream);
+/* Replaces quant.py:90 dequantize_group (batched, ragged): out = code * fp16(scale) + fp16(zero)
+ * in fp32 (product and sum rounded separately); max_len = the longest group (grid size hint). */
+int kvmix_dequantize_groups(const uint8_t* codes, const int64_t* offsets, int64_t n_groups, const float* scale,
+                            const float* zero, float* out, int64_t max_len, void* stream);
 /* Replaces quant.py:96 pack_codes / :112 unpack_codes. n codes <-> ceil(n*b/8) bytes.
  * pack sets err_flag bit 1 if a code is out of range. */
 int kvmix_pack_codes(const uint8_t* codes, int64_t n, int32_t bitwidth, uint8_t* out, int32_t* err_flag,

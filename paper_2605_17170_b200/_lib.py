@@ -44,6 +44,7 @@ _SIGS = {
     "kvmix_decode_key_pages": ([_P, _I64, _I64, _I64, _P, _P], ctypes.c_int),
     "kvmix_decode_token_blocks": ([_P, _I64, _I64, _I32, _I64, _P, _P], ctypes.c_int),
     "kvmix_quantize_groups": ([_P, _P, _I64, _I32, _P, _P, _P, _P, _P], ctypes.c_int),
+    "kvmix_dequantize_groups": ([_P, _P, _I64, _P, _P, _P, _I64, _P], ctypes.c_int),
     "kvmix_pack_codes": ([_P, _I64, _I32, _P, _P, _P], ctypes.c_int),
     "kvmix_unpack_codes": ([_P, _I64, _I32, _P, _P], ctypes.c_int),
     "kvmix_write_prefill": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _I64, _P,

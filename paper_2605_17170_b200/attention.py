@@ -245,12 +245,18 @@ def flash_decode_layers_from_host(q_host: torch.Tensor, batch: DecodeBatch, out_
     return out_host
 
 
-def flash_decode(q, page_table, pool_view, split_len: int = 128, scale=None, variant: int = VARIANT_TENSOR_CORE):
+def flash_decode(q, page_table, pool_view, split_len: int = 128, scale=None, variant: int | None = None):
     """attention.py:175-218 drop-in: single-query decode over a partitioned page table.
 
     ``split_len`` is validated like the reference but the device kernel chooses its own
     bitwidth-homogeneous split (a page or 32 INT4 slots per tile); results are
     split-invariant up to float rounding, as the reference's are.
+
+    Precision follows the caller's dtype (``variant=None``): an fp32/fp64 q -- the
+    reference's own arithmetic -- runs the fp32-faithful CUDA-core kernel (fp32 dequant,
+    dot products and softmax; within the reference's own 1e-5 relative bar of its tests,
+    pkg/tests/test_attention.py:205-246); a bf16/f16 q runs the tensor-core hot path
+    (within the north_star's atol 2e-3 / rtol 1e-2), as ``flash_decode_batched`` does.
     """
     is_torch = isinstance(q, torch.Tensor)
     qn = q if is_torch else np.asarray(q, dtype=np.float32)
@@ -279,6 +285,12 @@ def flash_decode(q, page_table, pool_view, split_len: int = 128, scale=None, var
     pool._require_written(slots, pool_view.layer)
     batch = DecodeBatch(pool, n_q_heads=n_heads, tables=[slots])
     qd = (q if is_torch else torch.as_tensor(qn)).to(pool.device, torch.float32).reshape(1, n_heads, d)
-    out = flash_decode_batched(qd, batch, pool_view.layer, scale=scale, variant=variant)
+    if variant is None:
+        wide = (q.dtype in (torch.float32, torch.float64)) if is_torch else True  # numpy q is fp32 (above)
+        variant = VARIANT_SIMPLE if wide else VARIANT_TENSOR_CORE
+    qd = qd if variant == VARIANT_SIMPLE or not is_torch else q.to(pool.device).reshape(1, n_heads, d)
+    out = flash_decode_batched(qd, batch, pool_view.layer, out=torch.empty(qd.shape, dtype=torch.float32,
+                                                                             device=pool.device),
+                               scale=scale, variant=variant)
     res = out[0]
     return res if is_torch else res.cpu().numpy()

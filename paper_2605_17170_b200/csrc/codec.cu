@@ -235,6 +235,18 @@ __global__ void quantize_groups_kernel(const float* __restrict__ x, const int64_
   }
 }
 
+// thread per element (quant.py:90-93): code * fp16(scale) + fp16(zero), the product and
+// the sum rounded separately like numpy's fp32 expression (no contraction to an FMA).
+__global__ void dequantize_groups_kernel(const uint8_t* __restrict__ codes, const int64_t* __restrict__ offsets,
+                                         int64_t n_groups, const float* __restrict__ scale,
+                                         const float* __restrict__ zero, float* __restrict__ out) {
+  const int64_t gi = blockIdx.y;
+  const int64_t lo = offsets[gi], hi = offsets[gi + 1];
+  const float s = __half2float(__float2half_rn(scale[gi])), z = __half2float(__float2half_rn(zero[gi]));
+  for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __fadd_rn(__fmul_rn((float)codes[i], s), z);
+}
+
 // thread per output byte (quant.py:96-109)
 __global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t n, int bits, uint8_t* __restrict__ out,
                                   int32_t* err) {
@@ -623,6 +635,16 @@ extern "C" int kvmix_quantize_groups(const float* x, const int64_t* offsets, int
                                                                                             bits, codes, scale, zero,
                                                                                             err);
   return check_launch("quantize_groups");
+}
+
+extern "C" int kvmix_dequantize_groups(const uint8_t* codes, const int64_t* offsets, int64_t n_groups,
+                                       const float* scale, const float* zero, float* out, int64_t max_len,
+                                       void* stream) {
+  if (n_groups == 0) return KVMIX_OK;
+  if (n_groups > 65535) return fail(KVMIX_EINVAL, "at most 65535 groups per call");
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((max_len + 127) / 128, 64)), (unsigned)n_groups);
+  dequantize_groups_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(codes, offsets, n_groups, scale, zero, out);
+  return check_launch("dequantize_groups");
 }
 
 extern "C" int kvmix_pack_codes(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out, int32_t* err,

@@ -121,34 +121,92 @@ def decode_token_blocks_device(blocks: torch.Tensor, head_dim: int, bitwidth: in
 
 
 # ---- reference API ------------------------------------------------------------------
+class _Staging:
+    """Per-device pinned host + device byte buffers for the single-group entry points: one
+    upload, the kernel and one download per call, one stream sync (the reference's per-group
+    API is called in tight loops, pkg/tests/test_acceptance.py:92-112)."""
+
+    _by_dev: dict = {}
+
+    def __init__(self, dev: torch.device):
+        self.dev = dev
+        self.cap = 0
+        self.grow(1 << 16)
+
+    def grow(self, n: int) -> None:
+        if n > self.cap:
+            self.cap = max(n, 2 * self.cap)
+            self.h = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
+            self.hn = self.h.numpy()
+            self.d = torch.empty(self.cap, dtype=torch.uint8, device=self.dev)
+
+    @classmethod
+    def get(cls) -> "_Staging":
+        dev = _lib.require_cuda()
+        st = cls._by_dev.get(dev.index)
+        if st is None:
+            st = cls._by_dev[dev.index] = _Staging(dev)
+        return st
+
+    def roundtrip(self, n_up: int, lo: int, hi: int, launch) -> np.ndarray:
+        """Upload h[:n_up], run launch(device base address), return a copy of d[lo:hi]."""
+        self.d[:n_up].copy_(self.h[:n_up], non_blocking=True)
+        launch(self.d.data_ptr())
+        self.h[lo:hi].copy_(self.d[lo:hi], non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self.hn[lo:hi].copy()
+
+
+def _align(n: int) -> int:
+    return (n + 15) & ~15
+
+
 def quantize_group(values, bitwidth: int) -> QuantGroup:
-    """quant.py:64-87."""
+    """quant.py:64-87 (one K-codec launch, kvmix_quantize_groups)."""
     if bitwidth not in (2, 4):
         raise ValidationError(f"unsupported bitwidth {bitwidth}")
     values = np.asarray(values, dtype=np.float32)
     if values.ndim != 1 or values.size == 0:
         raise ValidationError("values must be a non-empty 1-D vector")
-    x = _dev(values)
-    dev = x.device
-    offsets = torch.tensor([0, values.size], dtype=torch.int64, device=dev)
-    codes = torch.empty(values.size, dtype=torch.uint8, device=dev)
-    sz = torch.empty(2, dtype=torch.float32, device=dev)
-    err = _ErrFlag()
-    _lib.check(lib.kvmix_quantize_groups(x.data_ptr(), offsets.data_ptr(), 1, bitwidth, codes.data_ptr(),
-                                         sz.data_ptr(), sz.data_ptr() + 4, err.t.data_ptr(), _lib.stream()))
-    if err.value() & 1:
+    n = values.size
+    # staging: [offsets i64 x2 | err i32 | scale f32 | zero f32 | pad | x f32[n] | codes u8[n]]
+    ox, oc = 32, 32 + _align(4 * n)
+    st = _Staging.get()
+    st.grow(oc + n)
+    st.hn[:16].view(np.int64)[:] = (0, n)
+    st.hn[16:20].view(np.int32)[0] = 0
+    st.hn[ox:ox + 4 * n].view(np.float32)[:] = values
+
+    def launch(base):
+        _lib.check(lib.kvmix_quantize_groups(base + ox, base, 1, bitwidth, base + oc, base + 20, base + 24, base + 16,
+                                             _lib.stream()))
+
+    out = st.roundtrip(oc, 16, oc + n, launch)  # header + x up; err, scale, zero (and codes) down
+    err, s, z = int(out[:4].view(np.int32)[0]), float(out[4:8].view(np.float32)[0]), float(out[8:12].view(np.float32)[0])
+    if err & 1:
         raise ValidationError("values must be finite")
-    s, z = sz.cpu().numpy()
-    return QuantGroup(codes=codes.cpu().numpy(), scale=float(s), zero_offset=float(z), bitwidth=bitwidth,
-                      group_len=int(values.size))
+    return QuantGroup(codes=out[oc - 16:oc - 16 + n].copy(), scale=s, zero_offset=z, bitwidth=bitwidth, group_len=n)
 
 
 def dequantize_group(group: QuantGroup) -> np.ndarray:
-    """quant.py:90-93: code * scale + zero with fp16-narrowed params."""
-    codes = _dev(np.asarray(group.codes, dtype=np.float32))
-    s = torch.tensor(group.scale, dtype=torch.float32).half().float().item()
-    z = torch.tensor(group.zero_offset, dtype=torch.float32).half().float().item()
-    return (codes * s + z).cpu().numpy()
+    """quant.py:90-93: code * scale + zero with fp16-narrowed params (kvmix_dequantize_groups)."""
+    codes = np.asarray(group.codes, dtype=np.uint8).reshape(-1)
+    n = codes.size
+    if n == 0:
+        return np.zeros(0, np.float32)
+    # staging: [offsets i64 x2 | scale f32 | zero f32 | pad | codes u8[n] | out f32[n]]
+    oc = 32
+    oo = oc + _align(n)
+    st = _Staging.get()
+    st.grow(oo + 4 * n)
+    st.hn[:16].view(np.int64)[:] = (0, n)
+    st.hn[16:24].view(np.float32)[:] = (group.scale, group.zero_offset)
+    st.hn[oc:oc + n] = codes
+
+    def launch(base):
+        _lib.check(lib.kvmix_dequantize_groups(base + oc, base, 1, base + 16, base + 20, base + oo, n, _lib.stream()))
+
+    return st.roundtrip(oo, oo, oo + 4 * n, launch).view(np.float32)
 
 
 def pack_codes(codes, bitwidth: int) -> bytes:

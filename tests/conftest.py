@@ -22,6 +22,10 @@ import __graft_entry__  # noqa: E402
 __graft_entry__.build()
 
 
+# the vendored reference suite runs in its own pytest process (tests/test_ref_suite.py)
+collect_ignore_glob = ["ref_suite/*"]
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 device")
 

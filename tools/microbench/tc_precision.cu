@@ -44,35 +44,38 @@ static void run(uint16_t Am[16][16], uint16_t Bm[16][8], float Cm[16][8]) {
     Cm[g + 8][2 * q] = C[lane * 4 + 2]; Cm[g + 8][2 * q + 1] = C[lane * 4 + 3];
   }
 }
+static void sweep(int mode, int pos) {
+  // mode 0: subnormal, all A of a row at bit position pos (code << pos); mode 1: normal code * 2^(pos-10)
+  double worst = 0;
+  for (int ratio = 0; ratio <= 20; ratio += 4)
+    for (int t = 0; t < 200; ++t) {
+      uint16_t Am[16][16], Bm[16][8];
+      float Cm[16][8];
+      for (int r = 0; r < 16; ++r)
+        for (int kk = 0; kk < 16; ++kk) {
+          int code = rand() % 4;
+          Am[r][kk] = mode ? d2h((float)code * ldexpf(1.f, pos - 10)) : (uint16_t)(code << pos);
+        }
+      for (int n = 0; n < 8; ++n) {
+        Bm[0][n] = d2h((rand() / (float)RAND_MAX + 0.5f) * 20000.f);
+        for (int kk = 1; kk < 16; ++kk) Bm[kk][n] = d2h(((rand() / (float)RAND_MAX) * 2 - 1) * 20000.f * ldexpf(1.f, -ratio));
+      }
+      run(Am, Bm, Cm);
+      for (int r = 0; r < 16; ++r)
+        for (int n = 0; n < 8; ++n) {
+          double ref = 0, mx = 0;
+          for (int kk = 0; kk < 16; ++kk) { double p = h2d(Am[r][kk]) * h2d(Bm[kk][n]); ref += p; mx = fmax(mx, fabs(p)); }
+          if (mx == 0) continue;
+          double e = fabs(Cm[r][n] - ref) / mx;
+          if (e > worst) worst = e;
+        }
+    }
+  printf("%s codes at bit %d (uniform per row): worst |err| / max|product| = %.3e (2^%.1f)\n", mode ? "normal   " : "subnormal",
+         pos, worst, worst > 0 ? log2(worst) : -99.0);
+}
 int main() {
   srand(5);
-  for (int normal = 0; normal < 2; ++normal)
-    for (int ratio = 0; ratio <= 20; ratio += 4) {  // B of the small products = big B * 2^-ratio
-      double worst = 0;
-      for (int t = 0; t < 200; ++t) {
-        uint16_t Am[16][16], Bm[16][8];
-        float Cm[16][8];
-        for (int r = 0; r < 16; ++r)
-          for (int kk = 0; kk < 16; ++kk) {
-            int e = rand() % 4, code = rand() % 4;
-            Am[r][kk] = normal ? d2h((float)code * ldexpf(1.f, 2 * e - 10)) : (uint16_t)(code << (2 * e));
-          }
-        for (int n = 0; n < 8; ++n) {
-          Bm[0][n] = d2h((rand() / (float)RAND_MAX + 0.5f) * 20000.f);
-          for (int kk = 1; kk < 16; ++kk) Bm[kk][n] = d2h(((rand() / (float)RAND_MAX) * 2 - 1) * 20000.f * ldexpf(1.f, -ratio));
-        }
-        run(Am, Bm, Cm);
-        for (int r = 0; r < 16; ++r)
-          for (int n = 0; n < 8; ++n) {
-            double ref = 0, mx = 0;
-            for (int kk = 0; kk < 16; ++kk) { double p = h2d(Am[r][kk]) * h2d(Bm[kk][n]); ref += p; mx = fmax(mx, fabs(p)); }
-            if (mx == 0) continue;
-            double e = fabs(Cm[r][n] - ref) / mx;
-            if (e > worst) worst = e;
-          }
-      }
-      printf("%s A, small/big B = 2^-%2d: worst |err| / max|product| = %.3e (2^%.1f)\n", normal ? "normal   " : "subnormal",
-             ratio, worst, worst > 0 ? log2(worst) : -99.0);
-    }
+  for (int pos = 0; pos <= 8; pos += 2) sweep(0, pos);
+  for (int pos = 0; pos <= 8; pos += 2) sweep(1, pos);
   return 0;
 }
