@@ -281,13 +281,20 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t 
 // TokenBlock groups of consecutive tokens (quant.py:189-232), with the exact-fast code
 // path (FastQ).  The record is assembled in shared memory in the device layout and leaves
 // with coalesced 16-byte stores.
+#ifndef KVMIX_INT4_PRELOAD
+#define KVMIX_INT4_PRELOAD 0  // 1: INT4 token kernel issues K and V group loads together (measured 2% slower)
+#endif
+#ifndef KVMIX_K1_STAGES
+#define KVMIX_K1_STAGES 2
+#endif
 template <int D, typename T>
 struct PrefillCfg {
   static constexpr int ROWB = D * (int)sizeof(T);  // bytes per staged token row
   static constexpr int CHUNKS = ROWB / 16;
   static constexpr int SWZ = CHUNKS >= 8 ? 7 : CHUNKS - 1;
   static constexpr int TILE = G * ROWB;
-  static constexpr int SMEM = 4 * TILE + page_stride(D);  // 2 stages x (K, V) + the record
+  static constexpr int STAGES = KVMIX_K1_STAGES;  // 1: no intra-CTA prefetch, more resident CTAs
+  static constexpr int SMEM = 2 * STAGES * TILE + page_stride(D);  // stages x (K, V) + the record
 };
 
 template <int D, typename T>
@@ -330,6 +337,39 @@ __device__ __forceinline__ void load_pair(uint8_t* tile, int row, int c, float& 
   }
 }
 
+// Item cursor for the persistent page CTAs: item = lh * n_pages + p, lh = l * H + h,
+// advanced by the grid stride with precomputed carries (no 64-bit division per item).
+struct ItemCursor {
+  int p, h, l;
+  __device__ void init(int64_t item, int np, int H) {
+    const int64_t lh = item / np;
+    p = (int)(item - lh * np);
+    l = (int)(lh / H);
+    h = (int)(lh - (int64_t)l * H);
+  }
+  __device__ void advance(int dp, int dh, int dl, int np, int H) {
+    p += dp;
+    h += dh;
+    l += dl;
+    if (p >= np) {
+      p -= np;
+      ++h;
+    }
+    if (h >= H) {
+      h -= H;
+      ++l;
+    }
+  }
+};
+
+// K1 page kernel: write_prefill's INT2 data path (pool.py:228-262).  Persistent: CTA b runs
+// items b, b + grid, ... (item = (layer, kv head, page): one KeyPageBlock + the page's 32 INT2
+// V TokenBlocks); the K / V tiles of the next item stream in (cp.async, 2 stages) while this
+// one is encoded.  Each thread owns one 16 B column chunk of NPASS staged rows of both tiles
+// (fixed smem offsets); the rows' token ids and the page id are loaded two items ahead into
+// registers, so no copy or store waits on an index load.  (A variant that also ran the INT4
+// tokens as items of the same launch was slower: instruction-cache misses; another that
+// staged the index words through shared memory with cp.async lost ~8%.)
 template <int D, typename T>
 __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                             int64_t n_tokens, int64_t n_kv_heads, int64_t n_pages,
@@ -337,85 +377,128 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
                                                             const int32_t* __restrict__ page_ids,
                                                             uint8_t* __restrict__ int2_pool, int64_t pool_pages,
                                                             int32_t* err) {
-  // Persistent: CTA b runs items b, b + grid, ... (item = (layer, kv head, page)); the K / V
-  // tiles of the next item stream in (cp.async, 2 stages) while this one is encoded.
   using P = PrefillCfg<D, T>;
+  constexpr int RPP = 128 / P::CHUNKS;  // rows per copy pass
+  constexpr int NPASS = G / RPP;        // rows per thread and tile
+  static_assert(128 % P::CHUNKS == 0 && G % RPP == 0, "staging geometry");
   extern __shared__ __align__(16) uint8_t psm[];
-  uint8_t* srec = psm + 4 * P::TILE;
+  uint8_t* srec = psm + 2 * P::STAGES * P::TILE;
   const int tid = threadIdx.x;
-  // Row source addresses of an item, computed once per row (64 threads) into a 2-stage
-  // table, then every 16 B chunk copy is one table read + one cp.async.
-  __shared__ const uint8_t* rowp[2][2 * G];
-  auto rows = [&](int64_t item, int stg) {
-    if (tid < 2 * G) {
-      const int64_t p = item % n_pages, lh = item / n_pages;
-      const int64_t l = lh / n_kv_heads, h = lh % n_kv_heads;
-      const int tile = tid / G, r = tid % G;
-      const int t = page_tokens[p * G + r];
-      rowp[stg][tid] = reinterpret_cast<const uint8_t*>((tile ? values : keys) + ((l * n_tokens + t) * n_kv_heads + h) * D);
-    }
+  const int ch = tid % P::CHUNKS, r0 = tid / P::CHUNKS;
+  const int np = (int)n_pages, H = (int)n_kv_heads;
+  const int64_t grid = gridDim.x;
+  const int dp = (int)(grid % np), dlh = (int)(grid / np);
+  const int dh = dlh % H, dl = dlh / H;
+  ItemCursor cur, nxt, nn;  // this item, the one being fetched, the one whose indices load
+  cur.init(blockIdx.x, np, H);
+  nxt = cur;
+  nxt.advance(dp, dh, dl, np, H);
+  nn = nxt;
+  nn.advance(dp, dh, dl, np, H);
+  int tok_n[NPASS], tok_nn[NPASS], pid_n = 0, pid_nn = 0;
+  auto load_tok = [&](const ItemCursor& c, int64_t item, int (&tok)[NPASS], int& pid) {
+#pragma unroll
+    for (int j = 0; j < NPASS; ++j) tok[j] = item < n_items ? __ldg(page_tokens + (int64_t)c.p * G + r0 + RPP * j) : 0;
+    pid = item < n_items ? __ldg(page_ids + c.p) : 0;
   };
-  auto fetch = [&](int stg) {  // issue the item's 2 x 32 rows (table rowp[stg]) into stage stg
+  auto fetch = [&](const ItemCursor& c, const int (&tok)[NPASS], int stg) {
     uint8_t* Ks = psm + 2 * stg * P::TILE;
-#pragma unroll 4
-    for (int i = tid; i < 2 * G * P::CHUNKS; i += 128) {
-      const int tr = i / P::CHUNKS, ch = i % P::CHUNKS;  // tr = tile * 32 + row
-      cp_async16(staged<D, T>(Ks + (tr / G) * P::TILE, tr % G, 16 * ch), rowp[stg][tr] + 16 * ch);
+#pragma unroll
+    for (int j = 0; j < NPASS; ++j) {
+      const int r = r0 + RPP * j;
+      const int64_t off = (((int64_t)c.l * n_tokens + tok[j]) * H + c.h) * D;
+      uint8_t* dst = staged<D, T>(Ks, r, 16 * ch);
+      cp_async16(dst, reinterpret_cast<const uint8_t*>(keys + off) + 16 * ch);
+      cp_async16(dst + P::TILE, reinterpret_cast<const uint8_t*>(values + off) + 16 * ch);
     }
   };
-  int stg = 0;
+  int stg = 0, pid = 0;
   float kmx = 0.f, vmx = 0.f;  // largest key-page / V scales this thread stored (pool status)
   if (blockIdx.x < n_items) {
-    rows(blockIdx.x, 0);
-    __syncthreads();
-    fetch(0);
+    int tok0[NPASS];
+    load_tok(cur, blockIdx.x, tok0, pid);
+    if (P::STAGES == 2) fetch(cur, tok0, 0);
+    else
+#pragma unroll
+      for (int j = 0; j < NPASS; ++j) tok_n[j] = tok0[j];
   }
+  if (P::STAGES == 2) load_tok(nxt, blockIdx.x + grid, tok_n, pid_n);
   cp_async_commit();
-  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, stg ^= 1) {
-    const bool more = item + gridDim.x < n_items;
-    if (more) rows(item + gridDim.x, stg ^ 1);
-    __syncthreads();
-    if (more) fetch(stg ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();  // this item's tiles have landed (the next item's may still fly)
+  for (int64_t item = blockIdx.x; item < n_items; item += grid, stg ^= (P::STAGES - 1)) {
+    if constexpr (P::STAGES == 2) {
+      load_tok(nn, item + 2 * grid, tok_nn, pid_nn);
+      if (item + grid < n_items) fetch(nxt, tok_n, stg ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();  // this item's tiles have landed (the next item's may still fly)
+    } else {  // one stage: the other resident CTAs hide this one's load latency
+      fetch(cur, tok_n, 0);
+      cp_async_commit();
+      load_tok(nxt, item + grid, tok_nn, pid_nn);
+      cp_async_wait<0>();
+    }
     __syncthreads();
     uint8_t* Ks = psm + 2 * stg * P::TILE;
     uint8_t* Vs = Ks + P::TILE;
-    // KeyPageBlock channel c over the page's 32 tokens (threads 0..D-1) and V TokenBlock
-    // group j of token t (units D + 32 j + t); loops, not unrolled, around one encoder each.
+    // D work units of 64 elements: [0, D/2) = KeyPageBlock channels (2u, 2u+1) over the page's
+    // 32 tokens; [D/2, D) = V TokenBlock group j of tokens t and t + 16.  At d = 128 every
+    // thread runs one unit and warps 0-1 / 2-3 take the K / V halves (no divergence).
 #pragma unroll 1
-    for (int c = tid; c < D; c += 128) {
-      float x[G];
+    for (int u = tid; u < D; u += 128) {
+      if (u < D / 2) {
+        const int c = 2 * u;
+        float x0[G], x1[G];
 #pragma unroll
-      for (int i = 0; i < G; ++i) x[i] = load_one<D, T>(Ks, i, c);
-      uint32_t w[2], pz;
-      encode_group<2>(x, w, pz, err);
-      kmx = fmaxf(kmx, scale_of(pz));
+        for (int i = 0; i < G; ++i) load_pair<D, T>(Ks, i, c, x0[i], x1[i]);
+        uint32_t w0[2], w1[2], pz0, pz1;
+        encode_group<2>(x0, w0, pz0, err);
+        encode_group<2>(x1, w1, pz1, err);
+        kmx = fmaxf(kmx, fmaxf(scale_of(pz0), scale_of(pz1)));
 #pragma unroll
-      for (int b = 0; b < 8; ++b) srec[pg_kc_off(D, b, c)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
-      reinterpret_cast<uint16_t*>(srec + PG_KS(D))[pg_kp_idx(D, c)] = (uint16_t)(pz & 0xffffu);
-      reinterpret_cast<uint16_t*>(srec + PG_KZ(D))[pg_kp_idx(D, c)] = (uint16_t)(pz >> 16);
-    }
-#pragma unroll 1
-    for (int v = (tid + 128 - D % 128) % 128; v < G * (D / G); v += 128) {
-      const int j = v / G, t = v % G;
-      float x[G];
-      load_row_group<D, T>(Vs, t, j, x);  // 16-byte loads; rows t % 8 of a quarter warp differ: no conflicts
-      uint32_t w[2], pz;
-      encode_group<2>(x, w, pz, err);
-      vmx = fmaxf(vmx, scale_of(pz));
+        for (int b = 0; b < 8; ++b) {  // channels c, c + 1 are adjacent bytes of KC row b
+          const uint32_t sh = 8 * (b & 3);
+          *reinterpret_cast<uint16_t*>(srec + pg_kc_off(D, b, c)) =
+              (uint16_t)(((w0[b >> 2] >> sh) & 0xffu) | (((w1[b >> 2] >> sh) & 0xffu) << 8));
+        }
+        uint16_t* ks = reinterpret_cast<uint16_t*>(srec + PG_KS(D));
+        uint16_t* kz = reinterpret_cast<uint16_t*>(srec + PG_KZ(D));
+        ks[pg_kp_idx(D, c)] = (uint16_t)(pz0 & 0xffffu);
+        kz[pg_kp_idx(D, c)] = (uint16_t)(pz0 >> 16);
+        ks[pg_kp_idx(D, c + 1)] = (uint16_t)(pz1 & 0xffffu);
+        kz[pg_kp_idx(D, c + 1)] = (uint16_t)(pz1 >> 16);
+      } else {
+        const int v = u - D / 2, j = v / 16;
 #pragma unroll
-      for (int b = 0; b < 8; ++b)
-        srec[PG_VC(D) + pg_vc_off(D, t, 8 * j + b)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
-      reinterpret_cast<uint16_t*>(srec + PG_VS(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz & 0xffffu);
-      reinterpret_cast<uint16_t*>(srec + PG_VZ(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz >> 16);
+        for (int half = 0; half < 2; ++half) {
+          const int t = (v % 16) + 16 * half;
+          float x[G];
+          load_row_group<D, T>(Vs, t, j, x);  // 16-byte loads; rows t % 8 of a quarter warp differ: no conflicts
+          uint32_t w[2], pz;
+          encode_group<2>(x, w, pz, err);
+          vmx = fmaxf(vmx, scale_of(pz));
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            srec[PG_VC(D) + pg_vc_off(D, t, 8 * j + b)] = (uint8_t)((w[b >> 2] >> (8 * (b & 3))) & 0xffu);
+          reinterpret_cast<uint16_t*>(srec + PG_VS(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz & 0xffffu);
+          reinterpret_cast<uint16_t*>(srec + PG_VZ(D))[pg_vp_idx(D, t, j)] = (uint16_t)(pz >> 16);
+        }
+      }
     }
     __syncthreads();
-    const int64_t p = item % n_pages, lh = item / n_pages;
-    uint8_t* rec = int2_pool + (lh * pool_pages + page_ids[p]) * page_stride(D);
+    uint8_t* rec = int2_pool + (((int64_t)cur.l * H + cur.h) * pool_pages + pid) * page_stride(D);
     for (int i = tid; i < page_stride(D) / 16; i += 128)
       reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
     __syncthreads();  // srec and this stage are free
+    cur = nxt;
+    nxt = nn;
+    nn.advance(dp, dh, dl, np, H);
+#pragma unroll
+    for (int j = 0; j < NPASS; ++j) tok_n[j] = tok_nn[j];
+    if constexpr (P::STAGES == 2) {
+      pid = pid_n;
+      pid_n = pid_nn;
+    } else {
+      pid = pid_nn;
+    }
   }
   cp_async_wait<0>();
   publish_scales(err, kmx, vmx);
@@ -470,7 +553,7 @@ __global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ 
   if (i < n) {
     const int64_t t = tokens ? tokens[i] : i;
     const int64_t base = l * layer_stride + t * tok_stride + (int64_t)h * D + 32 * j;
-    vmx = encode_int4_group<D, T>(keys + base, values + base, st + tw * SS, nullptr, j, err);
+    vmx = encode_int4_group<D, T, KVMIX_INT4_PRELOAD>(keys + base, values + base, st + tw * SS, nullptr, j, err);
   }
   publish_scales(err, 0.f, vmx);
   __syncwarp();

@@ -8,4 +8,5 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 
 args = bench.parse()
-print(bench.measure_k1(args, torch.device("cuda", 0), 6448.4))
+import json  # noqa: E402
+print(json.dumps(bench.measure_k1(args, torch.device("cuda", 0), 6448.4), default=float))
