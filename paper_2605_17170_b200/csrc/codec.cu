@@ -401,12 +401,14 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     for (int j = 0; j < NPASS; ++j) tok[j] = item < n_items ? __ldg(page_tokens + (int64_t)c.p * G + r0 + RPP * j) : 0;
     pid = item < n_items ? __ldg(page_ids + c.p) : 0;
   };
+  const int64_t row_step = (int64_t)H * D;  // elements between consecutive tokens
   auto fetch = [&](const ItemCursor& c, const int (&tok)[NPASS], int stg) {
     uint8_t* Ks = psm + 2 * stg * P::TILE;
+    const int64_t base = ((int64_t)c.l * n_tokens * H + c.h) * D;
 #pragma unroll
     for (int j = 0; j < NPASS; ++j) {
       const int r = r0 + RPP * j;
-      const int64_t off = (((int64_t)c.l * n_tokens + tok[j]) * H + c.h) * D;
+      const int64_t off = base + (int64_t)tok[j] * row_step;
       uint8_t* dst = staged<D, T>(Ks, r, 16 * ch);
       cp_async16(dst, reinterpret_cast<const uint8_t*>(keys + off) + 16 * ch);
       cp_async16(dst + P::TILE, reinterpret_cast<const uint8_t*>(values + off) + 16 * ch);
@@ -436,7 +438,8 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
       load_tok(nxt, item + grid, tok_nn, pid_nn);
       cp_async_wait<0>();
     }
-    __syncthreads();
+    if (tid == 0) bulk_wait_read0();  // the previous item's record has left srec
+    __syncthreads();  // this stage's rows are visible; srec and the previous stage are free
     uint8_t* Ks = psm + 2 * stg * P::TILE;
     uint8_t* Vs = Ks + P::TILE;
     // D work units of 64 elements: [0, D/2) = KeyPageBlock channels (2u, 2u+1) over the page's
@@ -483,11 +486,12 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
         }
       }
     }
+    fence_proxy_async_smem();  // each thread's record writes, ordered before the bulk store's reads
     __syncthreads();
-    uint8_t* rec = int2_pool + (((int64_t)cur.l * H + cur.h) * pool_pages + pid) * page_stride(D);
-    for (int i = tid; i < page_stride(D) / 16; i += 128)
-      reinterpret_cast<uint4*>(rec)[i] = reinterpret_cast<const uint4*>(srec)[i];
-    __syncthreads();  // srec and this stage are free
+    if (tid == 0) {  // the record leaves with one TMA bulk store; srec is reused after it was read
+      bulk_s2g(int2_pool + (((int64_t)cur.l * H + cur.h) * pool_pages + pid) * page_stride(D), srec, page_stride(D));
+      bulk_commit();
+    }
     cur = nxt;
     nxt = nn;
     nn.advance(dp, dh, dl, np, H);
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     }
   }
   cp_async_wait<0>();
+  if (tid == 0) bulk_wait_read0();
   publish_scales(err, kmx, vmx);
 }
 
