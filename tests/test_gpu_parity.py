@@ -103,6 +103,26 @@ def test_cfg2_units_vs_oracle(cuda, out_dtype):
         print(f"cfg2 unit {i} ({out_dtype}): max abs err {err:.2e}, worst err/tol {worst:.3f}")
 
 
+@pytest.mark.parametrize("row", range(4))
+def test_cfg1_vs_oracle(cuda, row):
+    """BASELINE.json configs[0]: 1 layer, 8 q / 2 kv heads, d=128, batch 1, a 4K-token KV cache
+    with the reference-tagged bits (bench_data bits_4096, B = 2.5); bf16 q / out on the hot
+    path, and the fp32 drop-in API at the reference's own 1e-5 bar."""
+    n, H, Hq, d = 4096, 2, 8, 128
+    rng = np.random.default_rng(4096 + row)
+    bits = tagged_bits(n, row)
+    n2 = int((bits == 2).sum()) // 32 * 32
+    pair = Pair(total=n + 32, offset=n2, L=1, H=H, d=d)
+    k, v = kv_data(rng, 1, n, H, d)
+    pair.add("r0", bits, k, v)
+    q = bf16_exact(rng.standard_normal((1, Hq, d)))
+    out, refs = pair.decode(["r0"], q, 0)
+    err, worst = check(out[0], refs[0], what=f"cfg1 row {row}")
+    print(f"cfg1 row {row}: INT2 tokens {n2}/{n}, max abs err {err:.2e}, worst err/tol {worst:.3f}")
+    o32 = kv.flash_decode(q[0], pair.pool.table("r0"), pair.pool.view(0))
+    assert np.abs(o32 - refs[0]).max() / np.abs(refs[0]).max() < 1e-5
+
+
 @pytest.mark.parametrize("qmul", [3.0, 8.0])
 def test_sharp_softmax(cuda, qmul):
     """Large |q| (peaked attention): logit errors are no longer averaged away."""
