@@ -116,6 +116,14 @@ int kvmix_write_prefill(const void* keys, const void* values, int32_t dtype, int
 int kvmix_append_int4(const void* k, const void* v, int32_t dtype, int64_t n, int64_t n_layers_in, int64_t layer0,
                       int64_t n_layers, int64_t n_kv_heads, int64_t head_dim, const int32_t* int4_ids,
                       uint8_t* int4_pool, int64_t pool_int4, int32_t* err_flag, void* stream);
+/* The same with explicit element strides of the input: element (token i, layer l, head h, channel c)
+ * at k[l * layer_stride + i * tok_stride + h * head_dim + c] (kvmix_append_int4 is layer_stride =
+ * n_kv_heads * head_dim, tok_stride = n_layers_in * n_kv_heads * head_dim; a layer-major step
+ * buffer [n_layers_in][n][Hkv][d] is layer_stride = n * Hkv * d, tok_stride = Hkv * d). */
+int kvmix_append_int4_strided(const void* k, const void* v, int32_t dtype, int64_t n, int64_t n_layers_in,
+                              int64_t layer0, int64_t n_layers, int64_t n_kv_heads, int64_t head_dim,
+                              int64_t layer_stride, int64_t tok_stride, const int32_t* int4_ids, uint8_t* int4_pool,
+                              int64_t pool_int4, int32_t* err_flag, void* stream);
 
 /* Replaces pool.py:394 PoolView.gather and pool.py:264 read_slot (K5): decode slots[m]
  * of one layer into k_out, v_out f32 [m][Hkv][d]. */

@@ -50,6 +50,8 @@ _SIGS = {
     "kvmix_write_prefill": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P, _I64, _P, _I64, _P,
                              _I64, _P, _P], ctypes.c_int),
     "kvmix_append_int4": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P], ctypes.c_int),
+    "kvmix_append_int4_strided": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P],
+                                  ctypes.c_int),
     "kvmix_gather_dequant": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P], ctypes.c_int),
     "kvmix_gather_dequant_typed": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P],
                                    ctypes.c_int),

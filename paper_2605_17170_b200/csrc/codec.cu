@@ -809,11 +809,11 @@ extern "C" int kvmix_write_prefill(const void* keys, const void* values, int32_t
 
 template <typename T>
 static int launch_append(const void* k, const void* v, int64_t n, int64_t Lin, int64_t layer0, int64_t H, int64_t d,
-                         const int32_t* int4_ids, uint8_t* int4_pool, int64_t pool_int4, int32_t* err,
-                         cudaStream_t s) {
+                         int64_t layer_stride, int64_t tok_stride, const int32_t* int4_ids, uint8_t* int4_pool,
+                         int64_t pool_int4, int32_t* err, cudaStream_t s) {
   const int64_t tpc = 4 * (32 / (d / 32));  // tokens per CTA
   dim3 grid((unsigned)((n + tpc - 1) / tpc), (unsigned)H, (unsigned)Lin);
-  DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>((const T*)k, (const T*)v, n, H * D, Lin * H * D, H,
+  DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>((const T*)k, (const T*)v, n, layer_stride, tok_stride, H,
                                                               layer0, nullptr, int4_ids, int4_pool, pool_int4, err));
   return check_launch("append_int4");
 }
@@ -823,12 +823,24 @@ extern "C" int kvmix_append_int4(const void* k, const void* v, int32_t dtype, in
                                  uint8_t* int4_pool, int64_t pool_int4, int32_t* err, void* stream) {
   if (n == 0) return KVMIX_OK;
   if (layer0 < 0 || layer0 + Lin > L) return fail(KVMIX_EINVAL, "layer range outside the pool");
+  return kvmix_append_int4_strided(k, v, dtype, n, Lin, layer0, L, H, d, H * d, Lin * H * d, int4_ids, int4_pool,
+                                   pool_int4, err, stream);
+}
+
+extern "C" int kvmix_append_int4_strided(const void* k, const void* v, int32_t dtype, int64_t n, int64_t Lin,
+                                         int64_t layer0, int64_t L, int64_t H, int64_t d, int64_t layer_stride,
+                                         int64_t tok_stride, const int32_t* int4_ids, uint8_t* int4_pool,
+                                         int64_t pool_int4, int32_t* err, void* stream) {
+  if (n == 0) return KVMIX_OK;
+  if (layer0 < 0 || layer0 + Lin > L) return fail(KVMIX_EINVAL, "layer range outside the pool");
   cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ls = layer_stride, ts = tok_stride;
   switch (dtype) {
-    case KVMIX_F32: return launch_append<float>(k, v, n, Lin, layer0, H, d, int4_ids, int4_pool, pool_int4, err, s);
+    case KVMIX_F32: return launch_append<float>(k, v, n, Lin, layer0, H, d, ls, ts, int4_ids, int4_pool, pool_int4, err, s);
     case KVMIX_BF16:
-      return launch_append<__nv_bfloat16>(k, v, n, Lin, layer0, H, d, int4_ids, int4_pool, pool_int4, err, s);
-    case KVMIX_F16: return launch_append<__half>(k, v, n, Lin, layer0, H, d, int4_ids, int4_pool, pool_int4, err, s);
+      return launch_append<__nv_bfloat16>(k, v, n, Lin, layer0, H, d, ls, ts, int4_ids, int4_pool, pool_int4, err, s);
+    case KVMIX_F16:
+      return launch_append<__half>(k, v, n, Lin, layer0, H, d, ls, ts, int4_ids, int4_pool, pool_int4, err, s);
     default: return fail(KVMIX_EINVAL, "unsupported dtype");
   }
 }
