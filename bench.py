@@ -71,7 +71,7 @@ def parse():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--int2-frac", type=float, default=None, help="override: i.i.d. bits with this INT2 fraction")
     ap.add_argument("--ctas-per-sm", type=int, default=3, help="stream-K planner: resident CTAs per SM")
-    ap.add_argument("--int4-weight", type=float, default=0.9, help="stream-K planner: cost weight of INT4 bytes")
+    ap.add_argument("--int4-weight", type=float, default=0.8, help="stream-K planner: cost weight of INT4 bytes")
     ap.add_argument("--shards", type=int, default=None, help="heads mode: head shards (default: world size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -46,7 +46,7 @@ class DecodeStep:
     """
 
     def __init__(self, pool: MixedPrecisionPool, request_ids, n_q_heads: int, dtype=torch.bfloat16,
-                 max_new_tokens: int = 256, n_cta: int | None = None, int4_weight: float = 0.9,
+                 max_new_tokens: int = 256, n_cta: int | None = None, int4_weight: float = 0.8,
                  layer_chunk: int = 8, scale: float | None = None, fused_append: bool = False):
         cfg = pool.config
         if dtype not in (torch.float32, torch.bfloat16, torch.float16):

@@ -30,7 +30,7 @@ def _tile_bytes(n_pages: int, n_int4: int, page_stride: int, slot_stride: int, i
 
 
 def plan_stream(n_pages, n_int4, n_kv_heads: int, page_stride: int, slot_stride: int,
-                n_cta: int = 3 * NUM_SMS_B200, int4_weight: float = 0.9, tier_skew: float = 0.0,
+                n_cta: int = 3 * NUM_SMS_B200, int4_weight: float = 0.8, tier_skew: float = 0.0,
                 n_sm: int = NUM_SMS_B200):
     """Return (work int32 [n_pieces, 8], cta_ptr int32 [n_cta + 1], n_parts).
 
