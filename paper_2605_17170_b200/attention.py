@@ -30,7 +30,6 @@ from .pool import MixedPrecisionPool, PageTable, csr_tables, split_partitioned
 
 VARIANT_TENSOR_CORE = 0  # one warp per tile stream (QK + softmax + PV), 4 warps per CTA, 3 CTAs per SM
 VARIANT_SIMPLE = 1       # CUDA-core fp32 cross-check
-VARIANT_WARP_SPEC = 4    # warp-specialised QK / PV pairs, 8 warps per CTA, 2 CTAs per SM (slower today)
 CTAS_PER_SM = 3          # resident CTAs of the variant-0 kernel (168 regs x 128 threads, ~50 KB smem)
 
 

@@ -1078,171 +1078,6 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
 #endif
 }
 
-#ifdef KVMIX_MEASURE_VARIANTS
-// ====================================================================================
-// Variant 4 (measurement builds only, -DKVMIX_MEASURE_VARIANTS): warp-specialised tensor-core kernel.  A CTA holds NPAIR pairs of warps; in
-// pair p, warp p (QK) issues the TMA copies of the pair's tiles and computes the logits
-// S = QK^T (dequantised in registers), handing them (32 B per lane) to warp p + NPAIR (PV)
-// through the tile's own ring slot; the PV warp runs the online softmax and owns the
-// running max and the O / zero-point / softmax-sum accumulators.  The two halves of a
-// tile overlap across tiles, and each warp's dependency chains are half as long as in the
-// fused kernel.  Slot life: TMA (full) -> QK publishes S (pready) -> PV done (empty).
-#ifndef KVMIX_WS_STAGES
-#define KVMIX_WS_STAGES 4
-#endif
-#ifndef KVMIX_WS_MINB
-#define KVMIX_WS_MINB 2
-#endif
-constexpr int NPAIR = NW;                 // warp pairs per CTA (the merge treats pairs like warps)
-constexpr int WSTAGES = KVMIX_WS_STAGES;  // ring slots per pair; the QK warp prefetches WSTAGES - 2 tiles
-constexpr int PAREA = 1024;               // per slot: the tile's logits S (32 lanes x 8 fp32)
-
-template <int D>
-struct WsCfg {
-  static constexpr int SLOT = Cfg<D>::BUF + PAREA;
-  static constexpr int RING = NPAIR * WSTAGES * SLOT;
-  static constexpr int SMEM = RING + (D / 8 + 2) * 32 * 8 * 2 + Cfg<D>::QRAW;  // rings + q table (LO size) + raw q
-};
-
-template <int D, bool LO>
-__global__ void __launch_bounds__(2 * NPAIR * 32, KVMIX_WS_MINB) decode_ws_kernel(const DecodeArgs a) {
-  using C = Cfg<D>;
-  using W = WsCfg<D>;
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[NPAIR][WSTAGES], pready[NPAIR][WSTAGES], empty[NPAIR][WSTAGES];
-  __shared__ float sm_m[NPAIR * 8], sm_l[NPAIR * 8];
-  __shared__ int sm_flag;
-  __shared__ float sm_qscale;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-  const int g = lane >> 2, q = lane & 3;
-  const bool is_qk = warp < NPAIR;
-  const int pair = is_qk ? warp : warp - NPAIR;
-  uint8_t* ring = smem + pair * WSTAGES * W::SLOT;
-  uint64_t* qtab = reinterpret_cast<uint64_t*>(smem + W::RING);
-  if (threadIdx.x == 0) {
-    for (int p = 0; p < NPAIR; ++p)
-      for (int s = 0; s < WSTAGES; ++s) {
-        mbar_init(&full[p][s], 1);
-        mbar_init(&pready[p][s], 1);
-        mbar_init(&empty[p][s], 1);
-      }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  pdl_wait();
-  uint32_t kg = 0;  // tiles this pair has run so far (both warps count identically)
-
-  for (int piece = a.cta_ptr[blockIdx.x]; piece < a.cta_ptr[blockIdx.x + 1]; ++piece) {
-    const Unit u = load_unit(a, piece);
-    const int ntiles = u.thi - u.tlo;
-    const int nmine = ntiles > pair ? (ntiles - pair + NPAIR - 1) / NPAIR : 0;
-    auto tile_of = [&](int k) { return u.tlo + pair + k * NPAIR; };
-    float* qraw = reinterpret_cast<float*>(smem + W::RING + (D / 8 + 2) * 32 * 8 * 2);
-    const Bounds bnd = pool_bounds(a.pool_status);
-    stage_q<D>(a, u, qraw);
-    __syncthreads();
-    if (warp == 0) {
-      const float qs = build_qtab<D, LO>(qraw, qtab, lane, a.qscale, bnd.ek);
-      if (lane == 0) sm_qscale = qs;
-    }
-    __syncthreads();
-    const float qscale = sm_qscale;
-
-    if (is_qk) {
-      const uint8_t* kv2 = a.int2_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_pages) * (int64_t)C::PS;
-      const uint8_t* kv4 = a.int4_pool + ((a.layer * a.n_kv + u.kvh) * a.pool_int4) * (int64_t)C::SS;
-      auto meta_of = [&](int k) { return k < nmine ? tile_meta(a, u, tile_of(k), lane) : 0; };
-      auto do_issue = [&](int k, int meta) {  // tile k of this piece; its slot must be released by the PV warp
-        const uint32_t gk = kg + k;
-        const int s = gk % WSTAGES;
-        if (gk >= WSTAGES) mbar_wait(&empty[pair][s], ((gk / WSTAGES) - 1) & 1);
-        issue_tile<D>(u, tile_of(k), meta, ring + s * W::SLOT, &full[pair][s], lane, kv2, kv4);
-      };
-      for (int k = 0; k < WSTAGES - 2 && k < nmine; ++k) do_issue(k, meta_of(k));
-      int meta_next = meta_of(WSTAGES - 2);  // index loads run one tile ahead of their copies
-      const QFrag<D, LO> qf{qtab + lane};
-      const Softmax s0{0.f, 0.f, false, bnd.slack};  // the QK warp emits unshifted logits; the PV warp owns the max
-      for (int k = 0; k < nmine; ++k) {
-        const uint32_t gk = kg + k;
-        const int s = gk % WSTAGES;
-        uint8_t* buf = ring + s * W::SLOT;
-        mbar_wait(&full[pair][s], (gk / WSTAGES) & 1);
-        const int t = tile_of(k);
-        float sv[8];
-        if (t < u.npg) {
-          int2_qk<D, LO>(buf, qf, qscale, lane, s0, sv);
-        } else {
-          const int nv = min(32, u.n4 - 32 * (t - u.npg));
-          if (nv == 32) int4_qk<D, true, LO>(buf, 32, qf, qscale, lane, s0, sv);
-          else int4_qk<D, false, LO>(buf, nv, qf, qscale, lane, s0, sv);
-        }
-        float4* sa = reinterpret_cast<float4*>(buf + C::BUF) + 2 * lane;
-        sa[0] = make_float4(sv[0], sv[1], sv[2], sv[3]);
-        sa[1] = make_float4(sv[4], sv[5], sv[6], sv[7]);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pready[pair][s]);
-        if (k + WSTAGES - 2 < nmine) {
-          const int meta = meta_next;
-          meta_next = meta_of(k + WSTAGES - 1);
-          do_issue(k + WSTAGES - 2, meta);
-        }
-      }
-      kg += nmine;
-      __syncthreads();  // (A) every pair has finished the piece: the rings are idle
-      __syncthreads();  // (B) PV warps have written the merge scratch
-    } else {
-      Acc<D> acc;
-#pragma unroll
-      for (int m = 0; m < C::NCH; ++m) acc.o[m][0] = acc.o[m][1] = acc.o[m][2] = acc.o[m][3] = 0.f;
-      acc.zs[0] = acc.zs[1] = acc.zs[2] = acc.zs[3] = 0.f;
-      acc.zs2[0] = acc.zs2[1] = acc.zs2[2] = acc.zs2[3] = 0.f;
-      Softmax st{0.f, 0.f, false, bnd.slack};
-      for (int k = 0; k < nmine; ++k) {
-        const uint32_t gk = kg + k;
-        const int s = gk % WSTAGES;
-        const uint8_t* buf = ring + s * W::SLOT;
-        const uint32_t ph = (gk / WSTAGES) & 1;
-        mbar_wait(&pready[pair][s], ph);
-        mbar_wait(&full[pair][s], ph);  // already complete; makes the TMA bytes visible to this warp
-        const float4* sa = reinterpret_cast<const float4*>(buf + C::BUF) + 2 * lane;
-        const float4 x0 = sa[0], x1 = sa[1];
-        float sv[8] = {x0.x - st.m0, x0.y - st.m1, x0.z - st.m0, x0.w - st.m1,
-                       x1.x - st.m0, x1.y - st.m1, x1.z - st.m0, x1.w - st.m1};
-        uint32_t bP[2][2];
-        softmax_tile<D>(sv, st, acc, bP);
-        const int t = tile_of(k);
-        if (t < u.npg) {
-          int2_pv<D>(buf, bP, lane, acc);
-        } else {
-          const int nv = min(32, u.n4 - 32 * (t - u.npg));
-          if (nv == 32) int4_pv<D, true>(buf, 32, bP, lane, acc);
-          else int4_pv<D, false>(buf, nv, bP, lane, acc);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[pair][s]);
-      }
-      if (g == 0) {
-        sm_m[pair * 8 + 2 * q] = st.init ? st.m0 : -INFINITY;  // a pair without tiles contributes nothing
-        sm_m[pair * 8 + 2 * q + 1] = st.init ? st.m1 : -INFINITY;
-      }
-      const float l0 = __shfl_sync(0xffffffffu, acc.zs[0] + acc.zs2[0], 28 + q);  // ones rows (row 7)
-      const float l1 = __shfl_sync(0xffffffffu, acc.zs[1] + acc.zs2[1], 28 + q);
-      kg += nmine;
-      __syncthreads();  // (A)
-      store_warp_acc<D>(acc, reinterpret_cast<float*>(smem), pair, lane);
-      if (g == 0) {
-        sm_l[pair * 8 + 2 * q] = l0;
-        sm_l[pair * 8 + 2 * q + 1] = l1;
-      }
-      __syncthreads();  // (B)
-    }
-    finish_piece<D>(a, u, sm_m, sm_l, reinterpret_cast<const float*>(smem), &sm_flag);
-    __syncthreads();  // merge scratch (ring) and the q table are free for the next piece
-  }
-}
-
-#endif  // KVMIX_MEASURE_VARIANTS
-
 // ====================================================================================
 // Variant 1: simple CUDA-core kernel (fp32 dequant straight from HBM).  Slow; kept as
 // an independent on-GPU cross-check of the tensor-core kernel at full sizes.
@@ -1369,13 +1204,10 @@ static int launch_decode(const DecodeArgs& a, int64_t n_work, int variant, cudaS
       return launch_kernel(decode_mma_kernel<D, true, true, false>, a, n_work, Cfg<D>::SMEM, s);
     case 1: return launch_kernel(decode_simple_kernel<D>, a, n_work, NW * 8 * D * (int)sizeof(float), s);
 #ifdef KVMIX_MEASURE_VARIANTS
-    case 4:
-      if (a.q_dtype == KVMIX_F32) return launch_kernel(decode_ws_kernel<D, true>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
-      return launch_kernel(decode_ws_kernel<D, false>, a, n_work, WsCfg<D>::SMEM, s, 2 * NPAIR);
     case 2: return launch_kernel(decode_mma_kernel<D, false, true>, a, n_work, Cfg<D>::SMEM, s);
     case 3: return launch_kernel(decode_mma_kernel<D, true, false>, a, n_work, Cfg<D>::SMEM, s);
 #endif
-    default: return fail(KVMIX_EINVAL, "variant not built (2-4 need -DKVMIX_MEASURE_VARIANTS)");
+    default: return fail(KVMIX_EINVAL, "variant not built (2 and 3 need -DKVMIX_MEASURE_VARIANTS)");
   }
 }
 

@@ -78,32 +78,6 @@ def test_random_instances_vs_oracle(cuda):
     print(f"worst abs err over 200 instances: {worst:.2e}")
 
 
-def test_warp_specialised_variant(cuda):
-    """Variant 4 (QK warps hand logits to PV/softmax warps) gives the same results as the
-    default kernel (same math, same fp16 roundings; only the order of fp32 sums differs).
-    Measurement builds only (-DKVMIX_MEASURE_VARIANTS); the product library omits it."""
-    pool, t, *_ = build(1, 64, 1, 128, 0.5)
-    b = kv.DecodeBatch(pool, ["req"], n_q_heads=8)
-    try:
-        kv.flash_decode_batched(torch.zeros(1, 8, 128, device=cuda), b, 0, variant=4)
-    except kv.ValidationError:
-        pytest.skip("variant 4 not built (measurement builds only)")
-    rng = np.random.default_rng(7)
-    for i in range(40):
-        d = int(rng.choice([32, 64, 128]))
-        n_kv = int(rng.choice([1, 2, 4]))
-        H = n_kv * int(rng.choice([1, 4, 8]))
-        n = int(rng.integers(1, 3000))
-        pool, t, op, *_ = build(500 + i, n, n_kv, d, float(rng.uniform(0, 1)))
-        q = rng.standard_normal((H, d)).astype(np.float32)
-        ref = oatt.flash_decode_pool(q, op, "req", 0)
-        for n_cta in (2, 7, 296):
-            b = kv.DecodeBatch(pool, ["req"], n_q_heads=H, n_cta=n_cta)
-            o = kv.flash_decode_batched(torch.as_tensor(q, device=cuda)[None], b, 0, variant=4).cpu().numpy()[0]
-            ok, err = close(o, ref)
-            assert ok, (i, n_cta, err)
-
-
 def test_layers_from_host_matches_device_api(cuda):
     """The overlapped host-I/O step gives exactly the per-layer device API's outputs."""
     L, H, d = 5, 2, 128
