@@ -233,6 +233,11 @@ int kvmix_decode_tables(const int32_t* new_slots, int64_t batch, int64_t n_kv, c
 
 /* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
  * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */
+/* Replaces attention.py:32 attention_full (the calibration replay's dense attention, used by
+ * calibration.py:108-125 measure_raw): q f32 [n_q][n_heads][d], k / v f32 [n_k][n_kv_heads][d],
+ * out f32 [n_q][n_heads][d]; causal aligns the queries to the last n_q keys.  fp32, d in {32, 64, 128, 256}. */
+int kvmix_attention_full(const float* q, const float* k, const float* v, int64_t n_q, int64_t n_k, int64_t n_heads,
+                         int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, float* out, void* stream);
 int kvmix_merge_partials(const float* acc, const float* lse, const float* max_logit, int64_t n, int64_t d, float* out,
                          void* stream);
 

@@ -52,6 +52,7 @@ _SIGS = {
     "kvmix_append_int4": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P], ctypes.c_int),
     "kvmix_append_int4_strided": ([_P, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _I64, _P, _P],
                                   ctypes.c_int),
+    "kvmix_attention_full": ([_P, _P, _P, _I64, _I64, _I64, _I64, _I64, _F, _I32, _P, _P], ctypes.c_int),
     "kvmix_gather_dequant": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _P], ctypes.c_int),
     "kvmix_gather_dequant_typed": ([_P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64, _P, _P, _I32, _P],
                                    ctypes.c_int),

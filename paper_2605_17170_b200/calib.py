@@ -12,8 +12,8 @@ Here the fake quantization is the pool round trip itself -- the selected rows go
 K1 (``kvmix_write_prefill``) into a scratch pool and come back through K5
 (``kvmix_gather_dequant``), which reproduces the reference's quantize-dequantize images
 bit for bit (same routing: INT2 rows in sequence order form pages, the residual INT2 rows
-and the INT4 rows go per token at INT4) -- and the dense attention is fp32 matmuls on the
-device (TF32 off), with the MSE reduced in float64 like the reference.
+and the INT4 rows go per token at INT4) -- and the dense attention is one fused fp32 kernel (csrc/calib.cu,
+``kvmix_attention_full``), with the MSE reduced in float64 like the reference.
 """
 
 from __future__ import annotations
@@ -21,6 +21,8 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import _lib
+from ._lib import lib
 from .errors import ValidationError
 from .pool import MixedPrecisionPool, PoolConfig
 from .quant import GROUP_SIZE
@@ -70,7 +72,8 @@ def apply_mixed_quantization(k, v, row_bits, group_len: int = GROUP_SIZE, device
 
 def attention_full(q, k, v, scale=None, causal: bool = False):
     """attention.py:32-64 on the device, fp32: q [n_q, H, d], k / v [N, Hkv, d] -> [n_q, H, d].
-    With ``causal`` the queries are aligned to the last n_q key positions."""
+    With ``causal`` the queries are aligned to the last n_q key positions.  One fused launch
+    (``kvmix_attention_full``, csrc/calib.cu: flash-style fp32 tiles, online softmax)."""
     if q.dim() != 3 or k.dim() != 3 or v.dim() != 3 or k.shape != v.shape:
         raise ValidationError("Q/K/V must be rank-3 with matching K/V shapes")
     if q.shape[2] != k.shape[2]:
@@ -79,25 +82,21 @@ def attention_full(q, k, v, scale=None, causal: bool = False):
     n = k.shape[0]
     if H % k.shape[1]:
         raise ValidationError("query heads must be a multiple of kv heads")
+    if causal and n_q > n:
+        raise ValidationError("causal attention needs n_q <= N")
     if scale is None:
         scale = 1.0 / float(np.sqrt(d))
-    ratio = H // k.shape[1]
-    ke = k.repeat_interleave(ratio, dim=1).permute(1, 2, 0)  # [H, d, N]
-    ve = v.repeat_interleave(ratio, dim=1).permute(1, 0, 2)  # [H, N, d]
-    tf32 = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        logits = torch.bmm(q.permute(1, 0, 2), ke) * np.float32(scale)  # [H, n_q, N]
-        if causal:
-            off = n - n_q
-            if off < 0:
-                raise ValidationError("causal attention needs n_q <= N")
-            mask = torch.arange(n, device=q.device)[None, :] > (off + torch.arange(n_q, device=q.device))[:, None]
-            logits = logits.masked_fill(mask[None], float("-inf"))
-        p = torch.softmax(logits, dim=2)
-        return torch.bmm(p, ve).permute(1, 0, 2).contiguous()  # [n_q, H, d]
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = tf32
+    dev = q.device
+    q, k, v = (x.to(dev, torch.float32).contiguous() for x in (q, k, v))
+    dk = next((s for s in (32, 64, 128, 256) if s >= d), None)  # kernel head dims; zero channels change nothing
+    if dk is None:
+        raise ValidationError("head_dim above 256 is not supported on the device")
+    if dk != d:
+        q, k, v = (torch.nn.functional.pad(x, (0, dk - d)).contiguous() for x in (q, k, v))
+    out = torch.empty((n_q, H, dk), dtype=torch.float32, device=dev)
+    _lib.check(lib.kvmix_attention_full(q.data_ptr(), k.data_ptr(), v.data_ptr(), n_q, n, H, k.shape[1], dk,
+                                        float(np.float32(scale)), int(bool(causal)), out.data_ptr(), _lib.stream()))
+    return out if dk == d else out[..., :d].contiguous()
 
 
 def output_mse_per_head(o_ref, o_test) -> np.ndarray:

@@ -42,6 +42,30 @@ def test_attention_full_matches_oracle(cuda):
     assert np.allclose(got.cpu().numpy(), ref, rtol=1e-4, atol=1e-5)
 
 
+@pytest.mark.parametrize("d,H,Hkv,nq,nk,causal", [(32, 4, 4, 33, 33, True), (64, 8, 2, 200, 300, True),
+                                                   (128, 16, 2, 1024, 1024, True), (128, 8, 1, 17, 517, False),
+                                                   (64, 6, 3, 1, 95, True), (16, 2, 1, 10, 10, False),
+                                                   (256, 4, 2, 70, 70, True), (80, 4, 4, 40, 64, True)])
+def test_attention_kernel_vs_float64(cuda, d, H, Hkv, nq, nk, causal):
+    """The fused replay attention (csrc/calib.cu) against a float64 dense attention: ragged
+    tiles, GQA, causal and not, one query; fp32 accuracy."""
+    rng = np.random.default_rng(d + nq)
+    q = rng.standard_normal((nq, H, d)).astype(np.float32) * 2
+    k = rng.standard_normal((nk, Hkv, d)).astype(np.float32)
+    v = rng.standard_normal((nk, Hkv, d)).astype(np.float32)
+    got = calib.attention_full(*(torch.as_tensor(x, device=cuda) for x in (q, k, v)), causal=causal).cpu().numpy()
+    r = H // Hkv
+    kk = np.repeat(k.astype(np.float64), r, axis=1)
+    vv = np.repeat(v.astype(np.float64), r, axis=1)
+    logits = np.einsum("qhd,nhd->hqn", q.astype(np.float64), kk) / np.sqrt(d)
+    if causal:
+        mask = np.arange(nk)[None, :] > (nk - nq + np.arange(nq))[:, None]
+        logits[:, mask] = -np.inf
+    w = np.exp(logits - logits.max(-1, keepdims=True))
+    ref = np.einsum("hqn,nhd->qhd", w / w.sum(-1, keepdims=True), vv)
+    assert np.abs(got - ref).max() <= 2e-5 * max(1.0, np.abs(ref).max())
+
+
 def test_measure_raw_matches_oracle(cuda):
     caps = [_capture(s, n, 2, 8, 2, 64, 4) for s, n in ((21, 260), (22, 333))]
     got = calib.measure_raw(caps)
