@@ -51,6 +51,9 @@ constexpr int NW = KVMIX_NW;          // warps per CTA
 constexpr int STAGES = KVMIX_STAGES;  // ring depth per warp
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float RESCALE_SLACK = 8.f;  // largest lazy-rescale slack (log2 units), see softmax_p
+#ifndef KVMIX_INT4_RUNS
+#define KVMIX_INT4_RUNS 32  // > 32 never: INT4 tiles with more runs would be copied by per-lane cp.async (4: churned pools +10%, fresh pools -1.6%)
+#endif
 #ifndef KVMIX_Q2EXACT
 #define KVMIX_Q2EXACT 1  // INT2 key pages: q*s as an exact fp16 hi + lo pair (two MMAs per chunk)
 #endif
@@ -726,12 +729,23 @@ __device__ __forceinline__ void issue_tile(const Unit& u, int t, int meta, uint8
     const int prev = __shfl_up_sync(0xffffffffu, meta, 1);
     const bool start = lane < nv && (lane == 0 || meta != prev + 1);
     const uint32_t starts = __ballot_sync(0xffffffffu, start);
-    if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
-    __syncwarp();
-    if (start) {
-      const uint32_t later = starts & ~((2u << lane) - 1u);
-      const int end = later ? __ffs(later) - 1 : nv;
-      bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)meta * C::SS, (end - lane) * C::SS, bar);
+    if (__popc(starts) <= KVMIX_INT4_RUNS) {  // few runs of consecutive slots: one bulk copy each
+      if (lane == 0) mbar_expect_tx(bar, nv * C::SS);
+      __syncwarp();
+      if (start) {
+        const uint32_t later = starts & ~((2u << lane) - 1u);
+        const int end = later ? __ffs(later) - 1 : nv;
+        bulk_g2s(buf + lane * C::SS, kv4 + (int64_t)meta * C::SS, (end - lane) * C::SS, bar);
+      }
+    } else {  // scattered slots (after churn / decode appends): each lane copies its own record
+      if (lane < nv) {
+#pragma unroll
+        for (int c = 0; c < C::SS / 16; ++c)
+          cp_async16(buf + lane * C::SS + 16 * c, kv4 + (int64_t)meta * C::SS + 16 * c);
+        cp_async_mbar_arrive(bar);
+      }
+      __syncwarp();  // every lane's pending arrival is registered before the phase's own arrival
+      if (lane == 0) mbar_arrive(bar);
     }
   }
 }
