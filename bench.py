@@ -604,9 +604,7 @@ def run_decode(args, world, rank, local, device):
     traffic, traffic_src = committed_traffic()
     n2 = int(batch.csr["n_pages"].sum()) * 32
     ntok = int(batch.n_tokens.sum())
-    cfgd = config_dict(args, world)
-    cfgd.update({"stored_int2_fraction": n2 / ntok,
-                 "schedule": f"stream-K: {batch.n_cta} CTAs, {batch.n_pieces} pieces, {batch.n_parts} partials per layer"})
+    cfgd = config_dict(args, world)  # identical to the reference arm's (run facts go to "workload_stats")
     line = {
         "metric": METRIC, "value": world * args.batch / (ms_step / 1000.0), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -622,6 +620,9 @@ def run_decode(args, world, rank, local, device):
         "gpu_launches": args.steps * L,
         "clocks": clocks.summary(),
         "host": host_info(),
+        "workload_stats": {"stored_int2_fraction": n2 / ntok,
+                           "schedule": f"stream-K: {batch.n_cta} CTAs, {batch.n_pieces} pieces, "
+                                       f"{batch.n_parts} partials per layer"},
     }
     if churn is not None:
         line["churned"] = churn
