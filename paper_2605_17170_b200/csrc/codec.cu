@@ -281,6 +281,9 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t 
 // TokenBlock groups of consecutive tokens (quant.py:189-232), with the exact-fast code
 // path (FastQ).  The record is assembled in shared memory in the device layout and leaves
 // with coalesced 16-byte stores.
+#ifndef KVMIX_INT4_MINB
+#define KVMIX_INT4_MINB 12  // INT4 token kernel: 12 resident CTAs per SM (40 registers; measured best of 1 / 6 / 8 / 12)
+#endif
 #ifndef KVMIX_INT4_PRELOAD
 #define KVMIX_INT4_PRELOAD 0  // 1: INT4 token kernel issues K and V group loads together (measured 2% slower)
 #endif
@@ -536,7 +539,7 @@ __device__ __forceinline__ void load_lane(const T* __restrict__ p, float (&v)[D 
 // Input element (l, t, h, c) at (l * layer_stride + t * tok_stride + h * D + c); the
 // warp's slot records are staged in shared memory (device layout) and stored as 16 B words.
 template <int D, typename T>
-__global__ void __launch_bounds__(128) int4_tokens_kernel(const T* __restrict__ keys, const T* __restrict__ values,
+__global__ void __launch_bounds__(128, KVMIX_INT4_MINB) int4_tokens_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                           int64_t n, int64_t layer_stride, int64_t tok_stride,
                                                           int64_t n_kv_heads, int64_t layer0,
                                                           const int32_t* __restrict__ tokens,
