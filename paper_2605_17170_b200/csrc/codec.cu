@@ -290,13 +290,16 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ packed, int64_t 
 #ifndef KVMIX_K1_STAGES
 #define KVMIX_K1_STAGES 2
 #endif
+#if KVMIX_K1_STAGES != 2 && KVMIX_K1_STAGES != 3
+#error "KVMIX_K1_STAGES must be 2 or 3"
+#endif
 template <int D, typename T>
 struct PrefillCfg {
   static constexpr int ROWB = D * (int)sizeof(T);  // bytes per staged token row
   static constexpr int CHUNKS = ROWB / 16;
   static constexpr int SWZ = CHUNKS >= 8 ? 7 : CHUNKS - 1;
   static constexpr int TILE = G * ROWB;
-  static constexpr int STAGES = KVMIX_K1_STAGES;  // 1: no intra-CTA prefetch, more resident CTAs
+  static constexpr int STAGES = KVMIX_K1_STAGES;  // 2 or 3 items of K / V rows in flight per CTA
   static constexpr int SMEM = 2 * STAGES * TILE + page_stride(D);  // stages x (K, V) + the record
 };
 
@@ -392,13 +395,17 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
   const int64_t grid = gridDim.x;
   const int dp = (int)(grid % np), dlh = (int)(grid / np);
   const int dh = dlh % H, dl = dlh / H;
-  ItemCursor cur, nxt, nn;  // this item, the one being fetched, the one whose indices load
+  // cursors of this item and the next three: with 2 stages nxt is fetched while this one is
+  // encoded and nn's indices load; with 3 stages nn is fetched and n3's indices load
+  ItemCursor cur, nxt, nn, n3;
   cur.init(blockIdx.x, np, H);
   nxt = cur;
   nxt.advance(dp, dh, dl, np, H);
   nn = nxt;
   nn.advance(dp, dh, dl, np, H);
-  int tok_n[NPASS], tok_nn[NPASS], pid_n = 0, pid_nn = 0;
+  n3 = nn;
+  n3.advance(dp, dh, dl, np, H);
+  int tok_a[NPASS], tok_b[NPASS], pid_n = 0, pid_nn = 0, pid_n3 = 0;  // indices loaded ahead
   auto load_tok = [&](const ItemCursor& c, int64_t item, int (&tok)[NPASS], int& pid) {
 #pragma unroll
     for (int j = 0; j < NPASS; ++j) tok[j] = item < n_items ? __ldg(page_tokens + (int64_t)c.p * G + r0 + RPP * j) : 0;
@@ -419,27 +426,31 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
   };
   int stg = 0, pid = 0;
   float kmx = 0.f, vmx = 0.f;  // largest key-page / V scales this thread stored (pool status)
-  if (blockIdx.x < n_items) {
+  {
     int tok0[NPASS];
     load_tok(cur, blockIdx.x, tok0, pid);
-    if (P::STAGES == 2) fetch(cur, tok0, 0);
-    else
-#pragma unroll
-      for (int j = 0; j < NPASS; ++j) tok_n[j] = tok0[j];
+    if (blockIdx.x < n_items) fetch(cur, tok0, 0);
+    cp_async_commit();
+    if constexpr (P::STAGES == 3) {
+      load_tok(nxt, blockIdx.x + grid, tok0, pid_n);
+      if (blockIdx.x + grid < n_items) fetch(nxt, tok0, 1);
+      cp_async_commit();
+      load_tok(nn, blockIdx.x + 2 * grid, tok_a, pid_nn);
+    } else {
+      load_tok(nxt, blockIdx.x + grid, tok_a, pid_n);
+    }
   }
-  if (P::STAGES == 2) load_tok(nxt, blockIdx.x + grid, tok_n, pid_n);
-  cp_async_commit();
-  for (int64_t item = blockIdx.x; item < n_items; item += grid, stg ^= (P::STAGES - 1)) {
-    if constexpr (P::STAGES == 2) {
-      load_tok(nn, item + 2 * grid, tok_nn, pid_nn);
-      if (item + grid < n_items) fetch(nxt, tok_n, stg ^ 1);
+  for (int64_t item = blockIdx.x; item < n_items; item += grid, stg = stg + 1 == P::STAGES ? 0 : stg + 1) {
+    if constexpr (P::STAGES == 3) {
+      load_tok(n3, item + 3 * grid, tok_b, pid_n3);
+      if (item + 2 * grid < n_items) fetch(nn, tok_a, stg == 0 ? 2 : stg - 1);
+      cp_async_commit();
+      cp_async_wait<2>();  // this item's tiles have landed (the next two may still fly)
+    } else {
+      load_tok(nn, item + 2 * grid, tok_b, pid_nn);
+      if (item + grid < n_items) fetch(nxt, tok_a, stg ^ 1);
       cp_async_commit();
       cp_async_wait<1>();  // this item's tiles have landed (the next item's may still fly)
-    } else {  // one stage: the other resident CTAs hide this one's load latency
-      fetch(cur, tok_n, 0);
-      cp_async_commit();
-      load_tok(nxt, item + grid, tok_nn, pid_nn);
-      cp_async_wait<0>();
     }
     if (tid == 0) bulk_wait_read0();  // the previous item's record has left srec
     __syncthreads();  // this stage's rows are visible; srec and the previous stage are free
@@ -497,15 +508,13 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     }
     cur = nxt;
     nxt = nn;
-    nn.advance(dp, dh, dl, np, H);
+    nn = n3;
+    n3.advance(dp, dh, dl, np, H);
 #pragma unroll
-    for (int j = 0; j < NPASS; ++j) tok_n[j] = tok_nn[j];
-    if constexpr (P::STAGES == 2) {
-      pid = pid_n;
-      pid_n = pid_nn;
-    } else {
-      pid = pid_nn;
-    }
+    for (int j = 0; j < NPASS; ++j) tok_a[j] = tok_b[j];
+    pid = pid_n;
+    pid_n = pid_nn;
+    pid_nn = pid_n3;
   }
   cp_async_wait<0>();
   if (tid == 0) bulk_wait_read0();
