@@ -56,6 +56,22 @@ __device__ __forceinline__ void op(uint32_t (&a)[CH][4], float (&c)[CH][4], uint
     uint64_t* v = reinterpret_cast<uint64_t*>(c[i]);
     uint64_t bb = ((uint64_t)b1 << 32) | b0;
     asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(v[0]) : "l"(bb));
+  } else if constexpr (OP == 15) {  // e4m3x2 -> f16x2 conversion
+    uint32_t r;
+    asm volatile("{ .reg .b16 t; mov.b32 {t, _}, %1; cvt.rn.f16x2.e4m3x2 %0, t; }" : "=r"(r) : "r"(a[i][0]));
+    a[i][0] = r ^ b1;
+  } else if constexpr (OP == 16) {  // e2m1x2 -> f16x2 conversion
+    uint32_t r;
+    asm volatile("{ .reg .b8 t; mov.b32 {t, _, _, _}, %1; cvt.rn.f16x2.e2m1x2 %0, t; }" : "=r"(r) : "r"(a[i][0]));
+    a[i][0] = r ^ b1;
+  } else if constexpr (OP == 17) {  // e4m3x2 -> f16x2 conversion alone (output feeds the next)
+    asm volatile("{ .reg .b16 t; mov.b32 {t, _}, %0; cvt.rn.f16x2.e4m3x2 %0, t; }" : "+r"(a[i][0]));
+  } else if constexpr (OP == 18) {  // cvt and an independent LOP3 (shared pipe?)
+    asm volatile("{ .reg .b16 t; mov.b32 {t, _}, %0; cvt.rn.f16x2.e4m3x2 %0, t; }" : "+r"(a[i][0]));
+    asm volatile("lop3.b32 %0, %0, %1, %2, 0xEA;" : "+r"(a[i][1]) : "r"(b0), "r"(b1));
+  } else if constexpr (OP == 19) {  // cvt and an independent HADD2
+    asm volatile("{ .reg .b16 t; mov.b32 {t, _}, %0; cvt.rn.f16x2.e4m3x2 %0, t; }" : "+r"(a[i][0]));
+    asm volatile("sub.rn.f16x2 %0, %0, %1;" : "+r"(a[i][1]) : "r"(b0));
   } else if constexpr (OP == 14) {  // m16n8k8 f16 -> f32
     asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
                  : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
@@ -125,5 +141,10 @@ int main() {
   run<11>("ffma");
   run<12>("hfma2");
   run<13>("ffma2");
+  run<15>("cvt e4m3x2->f16x2 (+lop)");
+  run<16>("cvt e2m1x2->f16x2 (+lop)");
+  run<17>("cvt e4m3x2->f16x2 alone");
+  run<18>("cvt + independent lop3");
+  run<19>("cvt + independent hadd2");
   return 0;
 }
