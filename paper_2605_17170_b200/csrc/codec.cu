@@ -591,40 +591,82 @@ template <> __device__ __forceinline__ __half from_f32<__half>(float x) { return
 // K5 gather-dequant (pool.py:394-439): thread per (slot, head, channel) -> k/v in TO (f32 is
 // the reference's exact dequantized value; bf16 / f16 are its round-to-nearest image, the
 // input of an fp16 / bf16 prefill attention over the pool).
+// K5: one thread per (slot, kv head, 8-channel chunk) -- 8 K and 8 V values from one 8 / 16 B
+// load per field of the permuted record, written as one 16 B (f16 / bf16) or 32 B (f32) vector
+// each.  Values are fp32 code * scale + zero (exact: the product fits fp32), then rounded to TO.
+template <typename TO>
+__device__ __forceinline__ void store8(TO* p, const float (&x)[8]) {
+  if constexpr (sizeof(TO) == 4) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(x[0], x[1], x[2], x[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(x[4], x[5], x[6], x[7]);
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const TO a = from_f32<TO>(x[2 * e]), b = from_f32<TO>(x[2 * e + 1]);
+      w[e] = (uint32_t)(*reinterpret_cast<const uint16_t*>(&a)) | ((uint32_t)(*reinterpret_cast<const uint16_t*>(&b)) << 16);
+    }
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+__device__ __forceinline__ float half_of(uint32_t w, int hi) {
+  return __half2float(__ushort_as_half((unsigned short)(hi ? w >> 16 : w & 0xffffu)));
+}
+
 template <int D, typename TO>
-__global__ void gather_dequant_kernel(const uint8_t* __restrict__ int2_pool, const uint8_t* __restrict__ int4_pool,
-                                      int64_t pool_pages, int64_t pool_int4, int64_t offset, int64_t layer,
-                                      int64_t n_kv_heads, const int32_t* __restrict__ slots, int64_t m,
-                                      TO* __restrict__ k_out, TO* __restrict__ v_out) {
-  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= m * n_kv_heads * D) return;
-  const int c = (int)(idx % D);
-  const int64_t h = (idx / D) % n_kv_heads;
-  const int64_t i = idx / (D * n_kv_heads);
+__global__ void __launch_bounds__(256) gather_dequant_kernel(const uint8_t* __restrict__ int2_pool,
+                                                             const uint8_t* __restrict__ int4_pool, int64_t pool_pages,
+                                                             int64_t pool_int4, int64_t offset, int64_t layer,
+                                                             int64_t n_kv_heads, const int32_t* __restrict__ slots,
+                                                             int64_t m, TO* __restrict__ k_out, TO* __restrict__ v_out) {
+  constexpr int CH8 = D / 8;  // 8-channel chunks per (slot, head)
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * CH8) return;
+  const int h = blockIdx.y;
+  const int64_t i = idx / CH8;
+  const int c0 = 8 * (int)(idx % CH8);
   const int64_t slot = slots[i];
-  auto half_at = [](const uint8_t* p, int idx) {
-    return __half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(p)[idx]));
-  };
-  float kv, vv;
+  float kx[8], vx[8];
   if (slot < offset) {
-    const int64_t page = slot / G;
     const int row = (int)(slot % G);
-    const uint8_t* rec = int2_pool + ((layer * n_kv_heads + h) * pool_pages + page) * page_stride(D);
-    const uint32_t kc = (rec[pg_kc_off(D, row >> 2, c)] >> (2 * (row & 3))) & 3u;
-    kv = __fmaf_rn((float)kc, half_at(rec + PG_KS(D), pg_kp_idx(D, c)), half_at(rec + PG_KZ(D), pg_kp_idx(D, c)));
-    const uint32_t vc = (rec[PG_VC(D) + pg_vc_off(D, row, c >> 2)] >> (2 * (c & 3))) & 3u;
-    const int pj = pg_vp_idx(D, row, c / G);
-    vv = __fmaf_rn((float)vc, half_at(rec + PG_VS(D), pj), half_at(rec + PG_VZ(D), pj));
+    const uint8_t* rec = int2_pool + ((layer * n_kv_heads + h) * pool_pages + slot / G) * page_stride(D);
+    const uint2 kc = *reinterpret_cast<const uint2*>(rec + pg_kc_off(D, row >> 2, c0));  // channels c0 .. c0+7
+    const uint4 ks = *reinterpret_cast<const uint4*>(rec + PG_KS(D) + 2 * (pg_kp_idx(D, c0) & ~7));
+    const uint4 kz = *reinterpret_cast<const uint4*>(rec + PG_KZ(D) + 2 * (pg_kp_idx(D, c0) & ~7));
+    const uint32_t ksw[4] = {ks.x, ks.y, ks.z, ks.w}, kzw[4] = {kz.x, kz.y, kz.z, kz.w};
+    const int sh = 2 * (row & 3);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t code = (((e < 4 ? kc.x : kc.y) >> (8 * (e & 3) + sh)) & 3u);
+      const int pos = pg_kp_idx(D, c0 + e) & 7;
+      kx[e] = __fmaf_rn((float)code, half_of(ksw[pos >> 1], pos & 1), half_of(kzw[pos >> 1], pos & 1));
+    }
+    const uint32_t vb0 = rec[PG_VC(D) + pg_vc_off(D, row, c0 >> 2)], vb1 = rec[PG_VC(D) + pg_vc_off(D, row, (c0 >> 2) + 1)];
+    const int pj = pg_vp_idx(D, row, c0 / G);
+    const float vs = half_of(reinterpret_cast<const uint16_t*>(rec + PG_VS(D))[pj], 0);
+    const float vz = half_of(reinterpret_cast<const uint16_t*>(rec + PG_VZ(D))[pj], 0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) vx[e] = __fmaf_rn((float)(((e < 4 ? vb0 : vb1) >> (2 * (e & 3))) & 3u), vs, vz);
   } else {
     const uint8_t* rec = int4_pool + ((layer * n_kv_heads + h) * pool_int4 + (slot - offset)) * slot_stride(D);
-    const int sh = 4 * (c & 1);
-    const uint32_t kc = (rec[sl_kc_off(D, c >> 1)] >> sh) & 15u;
-    kv = __fmaf_rn((float)kc, half_at(rec + SL_KS(D), c / G), half_at(rec + SL_KZ(D), c / G));
-    const uint32_t vc = (rec[SL_VC(D) + sl_vc_off(D, c >> 1)] >> sh) & 15u;
-    vv = __fmaf_rn((float)vc, half_at(rec + SL_VS(D), c / G), half_at(rec + SL_VZ(D), c / G));
+    const int j = c0 / G;
+    const uint32_t kc = *reinterpret_cast<const uint32_t*>(rec + sl_kc_off(D, c0 >> 1));  // payload bytes c0/2 ..+3
+    const float ks = half_of(reinterpret_cast<const uint16_t*>(rec + SL_KS(D))[j], 0);
+    const float kz = half_of(reinterpret_cast<const uint16_t*>(rec + SL_KZ(D))[j], 0);
+    const uint32_t v01 = *reinterpret_cast<const uint16_t*>(rec + SL_VC(D) + sl_vc_off(D, c0 >> 1));
+    const uint32_t v23 = *reinterpret_cast<const uint16_t*>(rec + SL_VC(D) + sl_vc_off(D, (c0 >> 1) + 2));
+    const uint32_t vc = v01 | (v23 << 16);
+    const float vs = half_of(reinterpret_cast<const uint16_t*>(rec + SL_VS(D))[j], 0);
+    const float vz = half_of(reinterpret_cast<const uint16_t*>(rec + SL_VZ(D))[j], 0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      kx[e] = __fmaf_rn((float)((kc >> (4 * e)) & 15u), ks, kz);
+      vx[e] = __fmaf_rn((float)((vc >> (4 * e)) & 15u), vs, vz);
+    }
   }
-  k_out[idx] = from_f32<TO>(kv);
-  v_out[idx] = from_f32<TO>(vv);
+  const int64_t o = (i * n_kv_heads + h) * D + c0;
+  store8<TO>(k_out + o, kx);
+  store8<TO>(v_out + o, vx);
 }
 
 }  // namespace kvmix
@@ -861,8 +903,7 @@ template <typename TO>
 static int launch_gather(const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4,
                          int64_t offset, int64_t layer, int64_t H, int64_t d, const int32_t* slots, int64_t m,
                          void* k_out, void* v_out, cudaStream_t s) {
-  const int64_t total = m * H * d;
-  const unsigned grid = (unsigned)((total + 255) / 256);
+  const dim3 grid((unsigned)((m * (d / 8) + 255) / 256), (unsigned)H);
   DISPATCH_D(d, gather_dequant_kernel<D, TO><<<grid, 256, 0, s>>>(int2_pool, int4_pool, pool_pages, pool_int4, offset,
                                                                    layer, H, slots, m, static_cast<TO*>(k_out),
                                                                    static_cast<TO*>(v_out)));

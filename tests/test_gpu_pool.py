@@ -322,3 +322,47 @@ def test_gather_device_typed(cuda):
     pool.free("r")
     with pytest.raises(kv.ValidationError):
         pool.gather_device(t.slots, 0)
+
+
+def test_prefix_gather_feeds_fp16_prefill_attention(cuda):
+    """PAPER.md 'Prefill': a matched prefix is gathered from the pool and dequantized into an
+    FP16 buffer (K5, gather_device) and handed to an FP16 prefill attention together with the
+    new tokens' q / k / v.  Here the consumer is PyTorch's fused SDPA (standing in for the paper's
+    FlashInfer kernel): the new tokens' outputs agree with a float64 attention over the
+    reference-dequantized prefix (oracle gather) and the same fp16 new k / v."""
+    import torch.nn.functional as F
+
+    from oracle import pool as opool
+
+    rng = np.random.default_rng(8)
+    L, H, Hq, d, n_pre, n_new = 2, 2, 8, 128, 3000, 200
+    pool = kv.MixedPrecisionPool(kv.PoolConfig(total_slots=6144, offset=3072, n_layers=L, n_kv_heads=H, head_dim=d))
+    op = opool.OraclePool(opool.Config(6144, 3072, L, H, d))
+    bits = np.where(rng.random(n_pre) < 0.7, 2, 4)
+    k, v = rand_kv(81, L, n_pre, H, d)
+    t = pool.alloc("pre", bits)
+    op.alloc("pre", bits)
+    pool.write_prefill(t, k, v)
+    op.write_prefill("pre", k, v)
+    layer = 1
+    kp, vp = pool.gather_device(t.slots, layer, torch.float16)  # [n_pre, H, d] fp16 prefix
+    ko, vo = op.gather(op.tables["pre"], layer)
+    qn = torch.randn(n_new, Hq, d, device=cuda).half()
+    kn = torch.randn(n_new, H, d, device=cuda).half()
+    vn = torch.randn(n_new, H, d, device=cuda).half()
+    kk = torch.cat([kp, kn]).repeat_interleave(Hq // H, dim=1).permute(1, 0, 2)[None]  # [1, Hq, N, d]
+    vv = torch.cat([vp, vn]).repeat_interleave(Hq // H, dim=1).permute(1, 0, 2)[None]
+    n = n_pre + n_new
+    mask = torch.arange(n, device=cuda)[None, :] <= (n_pre + torch.arange(n_new, device=cuda))[:, None]
+    out = F.scaled_dot_product_attention(qn.permute(1, 0, 2)[None], kk, vv, attn_mask=mask)[0].permute(1, 0, 2)
+    # float64 reference over the oracle's dequantized prefix and the same fp16 new tokens
+    K = np.concatenate([ko, kn.float().cpu().numpy()]).astype(np.float64)
+    V = np.concatenate([vo, vn.float().cpu().numpy()]).astype(np.float64)
+    Q = qn.float().cpu().numpy().astype(np.float64)
+    K, V = np.repeat(K, Hq // H, axis=1), np.repeat(V, Hq // H, axis=1)
+    lg = np.einsum("qhd,nhd->hqn", Q, K) / np.sqrt(d)
+    lg[:, ~mask.cpu().numpy()] = -np.inf
+    w = np.exp(lg - lg.max(-1, keepdims=True))
+    ref = np.einsum("hqn,nhd->qhd", w / w.sum(-1, keepdims=True), V)
+    err = np.abs(out.float().cpu().numpy() - ref)
+    assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), float(err.max())
