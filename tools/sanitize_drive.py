@@ -2,10 +2,11 @@
 
     compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize_drive.py
 
-K1 prefill (page + INT4 kernels, f32 / bf16), K6 device routing, K5 gather, the generic codec
-entry points, K2 decode (tensor-core kernel with stream-K splits and the fused last-arriver
-combine; the fp32-faithful kernel), the K4 fused append, K7 device tables + the DecodeStep
-(eager, not graph-captured: the sanitizer tracks kernels), and merge_partials.  Sizes are
+K1 prefill (page + INT4 kernels, f32 / bf16), K6 device routing, K5 gather (f32 / f16 / bf16), the
+generic codec entry points, K2 decode (tensor-core kernel with stream-K splits and the fused
+last-arriver combine; the fp32-faithful kernel), the batched and the fused K4 append, K7 device
+tables + the DecodeStep (eager, not graph-captured: the sanitizer tracks kernels), the replay
+attention (f4) and merge_partials.  Sizes are
 small so each tool finishes in minutes; the outputs are checked against the oracle so a
 run that is silently wrong under instrumentation also fails.
 """
@@ -67,14 +68,22 @@ def main():
     out = kv.flash_decode(q[2].float().numpy(), pool.table("r2"), pool.view(0))  # fp32-faithful kernel
     assert np.abs(out - oatt.flash_decode_pool(q[2].float().numpy(), op, "r2", 0)).max() < 1e-4
 
-    # K4 fused append through DecodeStep (K7 device tables each step), eager
-    step = kv.DecodeStep(pool, rids, n_q_heads=Hq, max_new_tokens=4, n_cta=40)
-    for _ in range(2):
-        step.q_host.copy_(torch.randn(step.q_host.shape).to(step.q_host.dtype))
-        step.k_host.copy_(torch.randn(step.k_host.shape).to(step.k_host.dtype))
-        step.v_host.copy_(torch.randn(step.v_host.shape).to(step.v_host.dtype))
-        step.run(graph=False)
-        step.check()
+    # decode steps (K7 device tables each step), eager: batched append (K4 data half) + decode,
+    # and the fused form (K4 inside K2)
+    for fused in (False, True):
+        step = kv.DecodeStep(pool, rids, n_q_heads=Hq, max_new_tokens=4, n_cta=40, fused_append=fused)
+        for _ in range(2):
+            step.q_host.copy_(torch.randn(step.q_host.shape).to(step.q_host.dtype))
+            step.k_host.copy_(torch.randn(step.k_host.shape).to(step.k_host.dtype))
+            step.v_host.copy_(torch.randn(step.v_host.shape).to(step.v_host.dtype))
+            step.run(graph=False)
+            step.check()
+    # K5 typed gather and the replay attention (f2, f4)
+    for dt in (torch.float16, torch.bfloat16):
+        pool.gather_device(pool.table("r1").slots, 0, dt)
+    from paper_2605_17170_b200 import calib
+    qa = torch.randn(50, 8, d, device="cuda")
+    calib.attention_full(qa, torch.randn(70, 2, d, device="cuda"), torch.randn(70, 2, d, device="cuda"), causal=True)
     kv.merge_partials([kv.SplitPartial(acc=rng.standard_normal(d).astype(np.float32), lse=float(rng.standard_normal()),
                                        max_logit=float(rng.standard_normal())) for _ in range(3)])
     torch.cuda.synchronize()
