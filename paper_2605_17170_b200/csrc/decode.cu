@@ -389,7 +389,7 @@ __device__ __forceinline__ constexpr uint32_t F2(int e) { return 0x00030003u << 
 constexpr uint32_t N4L = 0x000F000Fu, N4H = 0x00F000F0u;  // INT4 low / high nibble of bytes 0, 2
 constexpr uint32_t ONES = 0x3C003C00u;  // (1.0, 1.0) fp16
 constexpr float P24 = 16777216.f, P22 = 4194304.f, P20 = 1048576.f, P18 = 262144.f;
-constexpr float P10 = 1024.f, P8 = 256.f, P6 = 64.f, P4 = 16.f;
+[[maybe_unused]] constexpr float P10 = 1024.f, P8 = 256.f, P6 = 64.f, P4 = 16.f;
 // Key codes enter QK as NORMAL fp16 numbers: (field | 1.0) - 1.0 = code * 2^(p-10) for a
 // field at bit p (one LOP3 + one exact HSUB2 per two codes).  The tensor core reduces
 // products of subnormal operands with ~13 bits of precision relative to the largest
@@ -400,6 +400,12 @@ constexpr float P10 = 1024.f, P8 = 256.f, P6 = 64.f, P4 = 16.f;
 #ifndef KVMIX_QKNORM
 #define KVMIX_QKNORM 1
 #endif
+// four e4m3 bytes -> two f16x2 words (bytes 0, 1 -> lo; bytes 2, 3 -> hi), hardware conversion
+__device__ __forceinline__ void cvt_e4m3x4(uint32_t v, uint32_t& lo, uint32_t& hi) {
+  asm("{\n .reg .b16 t0, t1;\n mov.b32 {t0, t1}, %2;\n cvt.rn.f16x2.e4m3x2 %0, t0;\n cvt.rn.f16x2.e4m3x2 %1, t1;\n}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(v));
+}
 __device__ __forceinline__ uint32_t kcode(uint32_t v, uint32_t mask) {
 #if KVMIX_QKNORM
   return hsub2u(lop_and_or(v, mask, ONES), ONES);
@@ -407,7 +413,10 @@ __device__ __forceinline__ uint32_t kcode(uint32_t v, uint32_t mask) {
   return v & mask;
 #endif
 }
-#if KVMIX_QKNORM
+#if KVMIX_QKCVT
+constexpr float KF0 = 512.f, KF1 = 128.f, KF2 = 512.f, KF3 = 128.f;  // INT2 key fields at 2^-9 / 2^-7 (cvt_e4m3x4)
+constexpr float KF4 = P6;                                              // INT4 key products at 2^-6
+#elif KVMIX_QKNORM
 constexpr float KF0 = P10, KF1 = P8, KF2 = P6, KF3 = P4;  // INT2 key field e at 2^(2e-10)
 constexpr float KF4 = P6;                                 // INT4 key products at 2^-6
 #else
@@ -416,7 +425,8 @@ constexpr float KF4 = P20;
 #endif
 
 // Q as B fragments of QK, fp16, NOT pre-scaled (bf16 q converts exactly).
-//  b2[I]  INT2 key pages, chunk I, lane q: channels cb = q*D/4 + 4I: (cb, cb+2) / (cb+1, cb+3)
+//  b2[I]  INT2 key pages, chunk I, lane q: channels cb = q*D/4 + 4I: (cb, cb+1) / (cb+2, cb+3)
+//         (round 1's subnormal / normal-code forms paired (cb, cb+2) / (cb+1, cb+3))
 //  b4[2j], b4[2j+1]  INT4 keys, group j, lane q: cb = 32j + 8q: (cb+1, cb+5) / (cb, cb+4) and
 //         (cb+2, cb+6) / (cb+3, cb+7)
 //  qz     (Q_2q, Q_2q+1) / 0 with Q_j = sum of q over channel group j (hi and lo fp16 parts)
@@ -480,13 +490,32 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
 #else
     const int P4 = 4 * (i >> 1), odd = i & 1;
 #endif
+#if KVMIX_QKCVT
+    const uint32_t w = kw[i];
+#else
     const uint32_t w = kw[i], x = w >> 8;
+#endif
     const uint64_t qi = qf.b2(i);
     const uint32_t s0 = ksw[P4 + odd], s1 = ksw[P4 + 2 + odd];
     const uint32_t h0 = hmul2u(lo32(qi), s0), h1 = hmul2u(hi32(qi), s1);
     const uint64_t qs = pack_b64(h0, h1);
+#if KVMIX_QKCVT
+    // The word holds the code bytes of channels cb..cb+3 (byte j = channel cb + j).  A byte with
+    // one field kept (value b < 16) read as e4m3 is exactly b * 2^-9, and the hardware e4m3x2 ->
+    // f16x2 conversion makes it a NORMAL fp16 number (full tensor-core precision, no subtraction):
+    // fields 0 / 2 masked at bits 0-1 give code * 2^-9, fields 1 / 3 at bits 2-3 give code * 2^-7.
+    // lo16 -> channels (cb, cb+1) = k-lo, hi16 -> (cb+2, cb+3) = k-hi; rows g / g+8 = fields 0 / 1
+    // (c0) and 2 / 3 (c1).
+    const uint32_t y = w >> 4;
+    uint32_t a00, a02, a01, a03, a10, a12, a11, a13;
+    cvt_e4m3x4(w & 0x03030303u, a00, a02);
+    cvt_e4m3x4(w & 0x0C0C0C0Cu, a01, a03);
+    cvt_e4m3x4(y & 0x03030303u, a10, a12);
+    cvt_e4m3x4(y & 0x0C0C0C0Cu, a11, a13);
+#else
     const uint32_t a00 = kcode(w, F2(0)), a01 = kcode(w, F2(1)), a02 = kcode(x, F2(0)), a03 = kcode(x, F2(1));
     const uint32_t a10 = kcode(w, F2(2)), a11 = kcode(w, F2(3)), a12 = kcode(x, F2(2)), a13 = kcode(x, F2(3));
+#endif
     mma16816_b64(c0, a00, a01, a02, a03, qs);
     mma16816_b64(c1, a10, a11, a12, a13, qs);
 #if KVMIX_Q2EXACT
@@ -828,8 +857,13 @@ __device__ __forceinline__ float build_qtab(const float* qraw, uint64_t* qtab, i
   for (int i = 0; i < C::NCH; ++i) {
     const int cb = q * (D / 4) + 4 * i;
     const float x0 = qv(cb), x1 = qv(cb + 1), x2 = qv(cb + 2), x3 = qv(cb + 3);
+#if KVMIX_QKCVT
+    put(i, pack_b64(pack_h2(x0, x1), pack_h2(x2, x3)));  // k-lo = channels (cb, cb+1), k-hi = (cb+2, cb+3)
+    if constexpr (LO) put(2 * QF::NCH + 2 + i, pack_b64(pack_h2(lo(x0), lo(x1)), pack_h2(lo(x2), lo(x3))));
+#else
     put(i, pack_b64(pack_h2(x0, x2), pack_h2(x1, x3)));
     if constexpr (LO) put(2 * QF::NCH + 2 + i, pack_b64(pack_h2(lo(x0), lo(x2)), pack_h2(lo(x1), lo(x3))));
+#endif
   }
   float qa = 0.f, qb = 0.f;  // Q_2q, Q_2q+1 (group sums, fp32)
 #pragma unroll

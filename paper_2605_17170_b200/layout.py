@@ -20,7 +20,7 @@ plus the page's 32 INT2 V TokenBlocks (quant.py:145-262) in slot order::
                  16-byte chunks are XOR-swizzled with (tau & 1)
   KS [8d, 10d)   key scales, fp16: lane q owns channels [q d/4, (q+1) d/4) in 8-channel chunks;
                  chunk i of lane q is chunk 4i + q; channel 8P + 4I + e of a chunk sits
-                 at 4(e&1) + 2I + (e>>1)
+                 at 4(e>>1) + 2I + (e&1)
   KZ [10d, 12d)  key zeros, same order
   VC [12d, 20d)  value codes: word ((ks*8 + g)*4 + q)*ng + j holds code byte
                  b = 8j + g of tokens [T0, T0+1, T1, T1+1], T0 = 8q + 2ks, T1 = T0 + 4
@@ -58,7 +58,7 @@ def _kp_pos(d: int, c: int) -> int:
     kb = d // 4  # channels per lane q
     q, o = divmod(c, kb)
     e = c & 3
-    return (((o >> 3) * 4 + q) << 3) | ((e & 1) << 2) | (((c >> 2) & 1) << 1) | (e >> 1)
+    return (((o >> 3) * 4 + q) << 3) | ((e >> 1) << 2) | (((c >> 2) & 1) << 1) | (e & 1)
 
 
 @functools.lru_cache(maxsize=None)
