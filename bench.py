@@ -568,6 +568,9 @@ def run_decode(args, world, rank, local, device):
     import paper_2605_17170_b200 as kv
 
     L = args.layers
+    # K1 first, on a fresh allocator state: re-allocated memory (after the decode legs free their
+    # pools) measured ~8% slower for this scattered-row gather (K1)
+    k1 = measure_k1(args, device, peak_hbm()[0]) if (rank == 0 and not args.no_k1 and not args.profile_only) else None
     sample_units = [(0, 0), (args.batch - 1, L - 1)] if rank == 0 else []
     pool, batch, q, out, bits, samples = build_workload(args, device, rank, sample_units=sample_units)
     timer = Timer(world, device)
@@ -626,8 +629,8 @@ def run_decode(args, world, rank, local, device):
     }
     if churn is not None:
         line["churned"] = churn
-    if not args.no_k1:
-        line["k1_prefill"] = measure_k1(args, device, peak)
+    if k1 is not None:
+        line["k1_prefill"] = k1
     if not args.no_cpu_baseline and world == 1 and samples:
         del pool, batch, q, out
         torch.cuda.empty_cache()
@@ -672,16 +675,18 @@ def measure_k1(args, device, peak) -> dict:
             it.data_ptr(), ii.data_ptr(), t4.size, pool.int2_pool.data_ptr(), pool.n_pages, pool.int4_pool.data_ptr(),
             pool.n_int4, pool.status.data_ptr(), _lib.stream()))
 
-    k1()
-    torch.cuda.synchronize()
-    reps = 5
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
+    for _ in range(3):  # first touches of the fresh pool and warm clocks
         k1()
-    e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    reps, times = 10, []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        k1()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
     route = measure_route(bits, cfg, device)
     bytes_in = 2 * k.numel() * k.element_size()
     bytes_out = L * H * (n_pages * pool.page_stride + n4 * 2 * kv.token_block_payload_bytes(d, 4))
