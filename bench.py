@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--ctas-per-sm", type=int, default=3, help="stream-K planner: resident CTAs per SM")
     ap.add_argument("--int4-weight", type=float, default=0.8, help="stream-K planner: cost weight of INT4 bytes")
     ap.add_argument("--shards", type=int, default=None, help="heads mode: head shards (default: world size)")
+    ap.add_argument("--combine", choices=["fused", "nccl"], default="fused",
+                    help="heads mode: head all-gather fused into the decode kernel's epilogue (stores into the "
+                         "ranks' symmetric-memory outputs over NVLink) or a per-layer NCCL all_gather_into_tensor")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-k1", action="store_true", help="skip the K1 quantize+pack (cfg3 slice) measurement")
@@ -760,13 +763,17 @@ def measure_route(bits, cfg, device) -> dict:
 def run_heads(args, world, rank, local, device):
     """cfg4: KV-head-parallel decode.  Rank r owns KV heads [r H/S, (r+1) H/S) (and their GQA q
     heads) of every request; page tables are replicated (every rank runs the same allocator
-    sequence, so slots agree -- slot addresses are head-agnostic, pool.py:108-110); per layer
-    each rank decodes its heads and one NCCL all-gather assembles the [B, Hq, d] output.
-    On one GPU (world 1) --shards S measures one shard of an S-way split (its attention only)."""
+    sequence, so slots agree -- slot addresses are head-agnostic, pool.py:108-110).  Per layer
+    each rank decodes its heads and the [B, Hq, d] output is assembled either inside the decode
+    kernel (--combine fused: its epilogue stores the head slice into every rank's symmetric-memory
+    output over NVLink, one device barrier per step) or by one NCCL all_gather_into_tensor per
+    layer (--combine nccl, the baseline).  On one GPU (world 1) --shards S measures one shard of
+    an S-way split; the fused combine then stores into the local [B, Hq, d] buffer only."""
     import torch
     import torch.distributed as dist
 
     import paper_2605_17170_b200 as kv
+    from paper_2605_17170_b200 import dist as kvdist
 
     S = args.shards or world
     H, L, d = args.kv_heads, args.layers, args.head_dim
@@ -776,8 +783,16 @@ def run_heads(args, world, rank, local, device):
     shard = rank if world > 1 else 0
     pool, batch, q, out, bits, _ = build_workload(args, device, rank, heads=(shard * hs, (shard + 1) * hs))
     hq = args.q_heads // S
-    gathered = torch.empty((L, world * args.batch, hq, d), dtype=out.dtype, device=device)
     timer = Timer(world, device)
+    fused = args.combine == "fused"
+    if fused and world > 1:
+        sg = kvdist.SymmetricHeadGather(L, args.batch, args.q_heads, d, dtype=out.dtype, device=device)
+        dests = [sg.layer(layer) for layer in range(L)]
+    elif fused:
+        full = torch.empty((L, args.batch, args.q_heads, d), dtype=out.dtype, device=device)
+        dests = [kvdist.HeadOutputs.local([full[layer]], head0=shard * hq) for layer in range(L)]
+    else:
+        gathered = torch.empty((L, world * args.batch, hq, d), dtype=out.dtype, device=device)
 
     def attn():
         for layer in range(L):
@@ -785,21 +800,34 @@ def run_heads(args, world, rank, local, device):
 
     def step():
         for layer in range(L):
-            kv.flash_decode_batched(q[layer], batch, layer, out=out[layer])
-            if world > 1:
-                dist.all_gather_into_tensor(gathered[layer], out[layer])
+            if fused:
+                kv.flash_decode_batched(q[layer], batch, layer, gather=dests[layer])
+            else:
+                kv.flash_decode_batched(q[layer], batch, layer, out=out[layer])
+                if world > 1:
+                    dist.all_gather_into_tensor(gathered[layer], out[layer])
+        if fused and world > 1:
+            sg.barrier()  # every rank's head slices have landed in every rank's output
 
     for _ in range(max(args.warmup, 1)):
         step()
     g_attn = capture(attn)
     ms_attn = timer(g_attn.replay, args.steps)
-    if world > 1:
+    if world > 1 and fused:
+        ms_step = timer(step, args.steps)  # eager: the symmetric-memory barrier stays outside a graph
+    elif world > 1 or fused:
         g_step = capture(step)
         for _ in range(2):
             g_step.replay()
         ms_step = timer(g_step.replay, args.steps)
     else:
         ms_step = ms_attn
+    if fused and world == 1:  # the shard's slice landed in the full-size output, equal to the plain decode's
+        torch.cuda.synchronize()
+        attn()
+        torch.cuda.synchronize()
+        if not torch.equal(full[:, :, :hq], out):
+            raise SystemExit("heads mode: the fused gather's output differs from the plain decode")
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
         return
@@ -807,9 +835,15 @@ def run_heads(args, world, rank, local, device):
     alg = algorithmic_bytes_per_layer(batch, hq, d)
     achieved = alg / (ms_attn / L / 1000.0) / 1e9
     cfgd = config_dict(args, world)
-    cfgd.update({"shards": S, "kv_heads_per_shard": hs, "measured_shard": shard,
-                 "note": ("one GPU holds one shard of an S-way split: the number is that shard's attention; the "
-                          "output all-gather is not measured") if world == 1 else "per-layer NCCL all_gather_into_tensor"})
+    if world == 1:
+        note = ("one GPU holds one shard of an S-way split: the number is that shard's attention"
+                + ("; the fused combine stores into the local [B, Hq, d] output only (no peers)" if fused
+                   else "; the output all-gather is not measured"))
+    else:
+        note = ("head slices stored by the decode kernel into every rank's symmetric-memory output over NVLink, "
+                "one device barrier per step" if fused else "per-layer NCCL all_gather_into_tensor")
+    cfgd.update({"shards": S, "kv_heads_per_shard": hs, "measured_shard": shard, "combine": args.combine,
+                 "note": note})
     line = {
         "metric": METRIC, "value": args.batch / (ms_step / 1000.0), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,

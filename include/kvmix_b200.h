@@ -184,9 +184,8 @@ int kvmix_route_tokens(const int8_t* bits, int64_t n, int32_t page_size, const i
  *     of the batch, see plan.py); the last CTA to finish a split unit merges its partials.
  *   counters [batch * Hkv] int32, zero before the first launch; every launch leaves them zero.
  *   variant: 0 = tensor-core kernel (mma.sync m16n8k16; plan with 3 CTAs per SM), 1 = simple
- *     CUDA-core kernel; measurement builds (-DKVMIX_MEASURE_VARIANTS) add 2 = data movement
- *     only, 3 = compute only on stale smem (output meaningless), 4 = warp-specialised
- *     tensor-core kernel (plan with 2 CTAs per SM)
+ *     CUDA-core kernel (fp32-faithful); measurement builds (-DKVMIX_MEASURE_VARIANTS) add
+ *     2 = data movement only, 3 = compute only on stale smem (output meaningless)
  *   pool_status: the pool status words (KVMIX_POOL_STATUS_*); NULL = operand bounds unknown
  *     (exact-max softmax and q pre-scaled for the largest finite scales: correct, slower).
  *   flags: KVMIX_DECODE_POOL_WRITTEN when a kernel that wrote this pool (write_prefill,
@@ -202,6 +201,23 @@ int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int32_t out_dt
                        const int32_t* int4_ids, const int32_t* int4_count, const int32_t* work,
                        const int32_t* cta_ptr, int64_t n_cta, float* partials, int32_t* counters, float scale,
                        int32_t variant, int32_t* pool_status, int32_t flags, void* stream);
+
+/* KV-head-parallel combine fused into the decode (cfg4; the all-gather of pool.py:108-110's
+ * head-agnostic slots + attention.py:198-201's kv = h // ratio): identical to kvmix_flash_decode,
+ * except that this rank's n_q_heads output heads are stored at head offset out_head0 of each of
+ * the n_outs (1..8) buffers outs[] = [batch][out_heads][d] (out_dtype): device addresses this
+ * process can store to -- its own gathered output and the peers' ones mapped over NVLink (e.g.
+ * torch symmetric memory).  The kernel's epilogue stores every finished head slice straight into
+ * every rank's buffer, so no separate all-gather runs; the caller orders the peers' reads after
+ * all ranks' launches (a symmetric-memory barrier).  outs is a HOST array of device addresses. */
+int kvmix_flash_decode_gather(const void* q, int32_t q_dtype, void* const* outs, int32_t n_outs, int64_t out_heads,
+                              int64_t out_head0, int32_t out_dtype, const uint8_t* int2_pool, const uint8_t* int4_pool,
+                              int64_t pool_pages, int64_t pool_int4, int64_t layer, int64_t n_kv_heads,
+                              int64_t head_dim, int64_t n_q_heads, int64_t batch, const int32_t* page_indptr,
+                              const int32_t* page_ids, const int32_t* int4_indptr, const int32_t* int4_ids,
+                              const int32_t* int4_count, const int32_t* work, const int32_t* cta_ptr, int64_t n_cta,
+                              float* partials, int32_t* counters, float scale, int32_t variant, int32_t* pool_status,
+                              int32_t flags, void* stream);
 
 /* K4 fused decode append (pool.py:284-306 append_decode_token data half + attention.py:175
  * flash_decode, one launch): the same as kvmix_flash_decode (variant 0) for one layer, where
@@ -231,13 +247,13 @@ int kvmix_decode_tables(const int32_t* new_slots, int64_t batch, int64_t n_kv, c
                         int64_t n_cta, int32_t* work, int32_t* cta_ptr, int32_t* n_parts, int32_t* scratch,
                         int32_t* err, void* stream);
 
-/* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
- * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */
 /* Replaces attention.py:32 attention_full (the calibration replay's dense attention, used by
  * calibration.py:108-125 measure_raw): q f32 [n_q][n_heads][d], k / v f32 [n_k][n_kv_heads][d],
  * out f32 [n_q][n_heads][d]; causal aligns the queries to the last n_q keys.  fp32, d in {32, 64, 128, 256}. */
 int kvmix_attention_full(const float* q, const float* k, const float* v, int64_t n_q, int64_t n_k, int64_t n_heads,
                          int64_t n_kv_heads, int64_t head_dim, float scale, int32_t causal, float* out, void* stream);
+/* Replaces attention.py:154 merge_partials for explicit partials (natural-log domain):
+ * acc [n][d], lse [n], max_logit [n] (device f32) -> out [d]. n >= 1. */
 int kvmix_merge_partials(const float* acc, const float* lse, const float* max_logit, int64_t n, int64_t d, float* out,
                          void* stream);
 

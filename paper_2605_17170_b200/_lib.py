@@ -58,6 +58,8 @@ _SIGS = {
                                    ctypes.c_int),
     "kvmix_flash_decode": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                             _P, _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
+    "kvmix_flash_decode_gather": ([_P, _I32, _P, _I32, _I64, _I64, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
+                                   _I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
     "kvmix_flash_decode_append": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P,
                                    _P, _P, _P, _P, _I64, _P, _P, _F, _P, _P, _I32, _P, _I32, _P], ctypes.c_int),
     "kvmix_decode_tables_smem": ([_I64, _I64], _I64),
@@ -93,6 +95,13 @@ def dtype_code(t: torch.Tensor) -> int:
         return _DT[t.dtype]
     except KeyError:
         raise ValidationError(f"unsupported dtype {t.dtype}") from None
+
+
+def dtype_code_of(dtype: torch.dtype) -> int:
+    try:
+        return _DT[dtype]
+    except KeyError:
+        raise ValidationError(f"unsupported dtype {dtype}") from None
 
 
 def ptr(t) -> int | None:

@@ -15,6 +15,7 @@ device, no host synchronisation.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 from typing import Sequence
@@ -121,7 +122,7 @@ class DecodeBatch:
 
 def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: torch.Tensor | None = None,
                          scale: float | None = None, variant: int = VARIANT_TENSOR_CORE,
-                         append: tuple | None = None) -> torch.Tensor:
+                         append: tuple | None = None, gather=None) -> torch.Tensor | None:
     """Decode attention for every request of ``batch`` at ``layer``.
 
     q: [B, n_q_heads, d] device tensor (f32/bf16/f16); returns out [B, n_q_heads, d]
@@ -132,6 +133,11 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
     ``batch.refresh()``) receives this layer's k/v, quantized inside the attention kernel
     by the warp that reads it, and the new token is attended to (pool.py:284-306 followed by
     attention.py:175-218, in one launch).
+
+    gather=``dist.HeadOutputs``: the KV-head-parallel combine fused into the kernel -- this
+    rank's head slice is stored at its head offset into every destination buffer (its own and
+    its peers', mapped over NVLink), so no all-gather follows (``out`` must be None; returns
+    None: the result is in the destinations once every rank's launch is done).
     """
     pool, cfg = batch.pool, batch.pool.config
     if q.dim() != 3 or q.shape[0] != batch.batch or q.shape[1] != batch.n_q_heads or q.shape[2] != cfg.head_dim:
@@ -143,7 +149,10 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
     if not q.is_contiguous():
         q = q.contiguous()
     if out is None:
-        out = torch.empty_like(q)
+        if gather is None:
+            out = torch.empty_like(q)
+    elif gather is not None:
+        raise ValidationError("out and gather are exclusive: the gather destinations are the output")
     elif (tuple(out.shape) != tuple(q.shape) or not out.is_contiguous() or out.device != pool.device
           or out.dtype not in (torch.float32, torch.bfloat16, torch.float16)):
         raise ValidationError(f"out must be a contiguous f32/bf16/f16 [{batch.batch}, {batch.n_q_heads}, "
@@ -153,6 +162,21 @@ def flash_decode_batched(q: torch.Tensor, batch: DecodeBatch, layer: int, out: t
     t = batch.csr
     # a pool writer launched just before may still be storing what this launch prefetches
     flags = _lib.DECODE_POOL_WRITTEN if pool._written is True or pool._written == layer else 0
+    if gather is not None:
+        if append is not None:
+            raise ValidationError("the fused head gather does not take a fused append (append first)")
+        gather.check(batch.batch, batch.n_q_heads, cfg.head_dim, pool.device)
+        ptrs = (ctypes.c_void_p * len(gather.ptrs))(*gather.ptrs)
+        _lib.check(lib.kvmix_flash_decode_gather(
+            q.data_ptr(), _lib.dtype_code(q), ctypes.cast(ptrs, ctypes.c_void_p), len(gather.ptrs), gather.out_heads,
+            gather.head0, _lib.dtype_code_of(gather.dtype), pool.int2_pool.data_ptr(), pool.int4_pool.data_ptr(), pool.n_pages,
+            pool.n_int4, layer, cfg.n_kv_heads, cfg.head_dim, batch.n_q_heads, batch.batch,
+            t["page_indptr"].data_ptr(), t["page_ids"].data_ptr(), t["int4_indptr"].data_ptr(),
+            t["int4_ids"].data_ptr(), None, batch.work.data_ptr(), batch.cta_ptr.data_ptr(), batch.n_cta,
+            batch.partials.data_ptr(), batch.counters.data_ptr(), float(scale), int(variant), pool.status.data_ptr(),
+            flags, _lib.stream()))
+        pool._written = False
+        return None
     if append is not None:
         k_new, v_new = append
         want = (batch.batch, cfg.n_kv_heads, cfg.head_dim)

@@ -82,10 +82,17 @@ struct Cfg {
   static constexpr int SMEM = NW * STAGES * BUF + QTAB + (MERGE_IN_RING ? 0 : MERGE) + QRAW;
 };
 
+constexpr int MAX_OUTS = 8;  // destinations of the fused head all-gather (one NVLink domain)
+
 struct DecodeArgs {
   const void* q;
   int q_dtype;
-  void* out;
+  // Outputs: head h of request b goes to element ((b * out_heads + out_head0 + h) * D + c) of
+  // every outs[0 .. n_outs): this process's own buffer and, for the KV-head-parallel combine,
+  // the peers' buffers mapped over NVLink (kvmix_flash_decode_gather).  Plain decode: one
+  // destination, out_heads = n_q, out_head0 = 0.
+  void* outs[MAX_OUTS];
+  int n_outs, out_heads, out_head0;
   int out_dtype;
   const uint8_t* int2_pool;
   const uint8_t* int4_pool;
@@ -147,9 +154,13 @@ __device__ __forceinline__ Unit load_unit(const DecodeArgs& a, int piece) {
 }
 
 __device__ __forceinline__ void store_out(const DecodeArgs& a, int64_t oi, float v) {
-  if (a.out_dtype == KVMIX_F32) reinterpret_cast<float*>(a.out)[oi] = v;
-  else if (a.out_dtype == KVMIX_BF16) reinterpret_cast<__nv_bfloat16*>(a.out)[oi] = __float2bfloat16(v);
-  else reinterpret_cast<__half*>(a.out)[oi] = __float2half(v);
+#pragma unroll
+  for (int p = 0; p < MAX_OUTS; ++p) {  // static indices: the pointers stay in the parameter bank
+    if (p >= a.n_outs) break;
+    if (a.out_dtype == KVMIX_F32) reinterpret_cast<float*>(a.outs[p])[oi] = v;
+    else if (a.out_dtype == KVMIX_BF16) reinterpret_cast<__nv_bfloat16*>(a.outs[p])[oi] = __float2bfloat16(v);
+    else reinterpret_cast<__half*>(a.outs[p])[oi] = __float2half(v);
+  }
 }
 
 // Piece epilogue shared by both variants (K3, the cross-split combine, is fused in):
@@ -162,7 +173,7 @@ template <int D>
 __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u, const float* sm_m,
                                              const float* sm_l, const float* sm_acc, int* sm_flag) {
   __syncthreads();
-  const int64_t obase = ((int64_t)u.b * a.n_q + (int64_t)u.kvh * a.gq) * D;
+  const int64_t obase = ((int64_t)u.b * a.out_heads + a.out_head0 + (int64_t)u.kvh * a.gq) * D;
   for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
     const int hh = i / D, c = i % D;
     float M = -INFINITY;
@@ -1290,7 +1301,8 @@ extern "C" int kvmix_merge_partials(const float* acc, const float* lse, const fl
   return check_launch("merge_partials");
 }
 
-static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
+static int flash_decode_impl(const void* q, int32_t q_dtype, void* const* outs, int32_t n_outs, int64_t out_heads,
+                             int64_t out_head0, int32_t out_dtype,
                              const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages, int64_t pool_int4,
                              int64_t layer, int64_t n_kv, int64_t d, int64_t n_q, int64_t batch,
                              const int32_t* page_indptr, const int32_t* page_ids, const int32_t* int4_indptr,
@@ -1305,11 +1317,19 @@ static int flash_decode_impl(const void* q, int32_t q_dtype, void* out, int32_t 
   if (batch <= 0 || n_cta <= 0 || n_cta > (1 << 20)) return fail(KVMIX_EINVAL, "empty batch or CTA schedule");
   if (!work || !cta_ptr || !counters) return fail(KVMIX_EINVAL, "work, cta_ptr and counters are required");
   if (q_dtype < 0 || q_dtype > 2 || out_dtype < 0 || out_dtype > 2) return fail(KVMIX_EINVAL, "bad dtype");
-  if (variant < 0 || variant > 4) return fail(KVMIX_EINVAL, "bad variant");
+  if (variant < 0 || variant > 3) return fail(KVMIX_EINVAL, "bad variant");
+  if (!outs || n_outs < 1 || n_outs > MAX_OUTS) return fail(KVMIX_EINVAL, "1 to 8 output buffers");
+  if (out_head0 < 0 || out_head0 + n_q > out_heads) return fail(KVMIX_EINVAL, "head slice outside the output");
   DecodeArgs a;
   a.q = q;
   a.q_dtype = q_dtype;
-  a.out = out;
+  for (int p = 0; p < MAX_OUTS; ++p) {
+    a.outs[p] = p < n_outs ? outs[p] : nullptr;
+    if (p < n_outs && !outs[p]) return fail(KVMIX_EINVAL, "null output buffer");
+  }
+  a.n_outs = n_outs;
+  a.out_heads = (int)out_heads;
+  a.out_head0 = (int)out_head0;
   a.out_dtype = out_dtype;
   a.int2_pool = int2_pool;
   a.int4_pool = int4_pool;
@@ -1357,9 +1377,25 @@ extern "C" int kvmix_flash_decode(const void* q, int32_t q_dtype, void* out, int
                                   const int32_t* work, const int32_t* cta_ptr, int64_t n_cta, float* partials,
                                   int32_t* counters, float scale, int32_t variant, int32_t* pool_status, int32_t flags,
                                   void* stream) {
-  return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
-                           batch, page_indptr, page_ids, int4_indptr, int4_ids, int4_count, work, cta_ptr, n_cta, partials,
-                           counters, scale, variant, nullptr, nullptr, 0, nullptr, pool_status, flags, stream);
+  return flash_decode_impl(q, q_dtype, &out, 1, n_q, 0, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer,
+                           n_kv, d, n_q, batch, page_indptr, page_ids, int4_indptr, int4_ids, int4_count, work, cta_ptr,
+                           n_cta, partials, counters, scale, variant, nullptr, nullptr, 0, nullptr, pool_status, flags,
+                           stream);
+}
+
+extern "C" int kvmix_flash_decode_gather(const void* q, int32_t q_dtype, void* const* outs, int32_t n_outs,
+                                         int64_t out_heads, int64_t out_head0, int32_t out_dtype,
+                                         const uint8_t* int2_pool, const uint8_t* int4_pool, int64_t pool_pages,
+                                         int64_t pool_int4, int64_t layer, int64_t n_kv, int64_t d, int64_t n_q,
+                                         int64_t batch, const int32_t* page_indptr, const int32_t* page_ids,
+                                         const int32_t* int4_indptr, const int32_t* int4_ids,
+                                         const int32_t* int4_count, const int32_t* work, const int32_t* cta_ptr,
+                                         int64_t n_cta, float* partials, int32_t* counters, float scale,
+                                         int32_t variant, int32_t* pool_status, int32_t flags, void* stream) {
+  return flash_decode_impl(q, q_dtype, outs, n_outs, out_heads, out_head0, out_dtype, int2_pool, int4_pool, pool_pages,
+                           pool_int4, layer, n_kv, d, n_q, batch, page_indptr, page_ids, int4_indptr, int4_ids,
+                           int4_count, work, cta_ptr, n_cta, partials, counters, scale, variant, nullptr, nullptr, 0,
+                           nullptr, pool_status, flags, stream);
 }
 
 extern "C" int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* out, int32_t out_dtype,
@@ -1371,7 +1407,8 @@ extern "C" int kvmix_flash_decode_append(const void* q, int32_t q_dtype, void* o
                                          int32_t* counters, float scale, const void* k_new, const void* v_new,
                                          int32_t kv_dtype, int32_t* pool_status, int32_t flags, void* stream) {
   if (!k_new || !v_new) return fail(KVMIX_EINVAL, "k_new / v_new are required");
-  return flash_decode_impl(q, q_dtype, out, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer, n_kv, d, n_q,
-                           batch, page_indptr, page_ids, int4_indptr, int4_ids, int4_count, work, cta_ptr, n_cta, partials,
-                           counters, scale, 0, k_new, v_new, kv_dtype, int4_pool, pool_status, flags, stream);
+  return flash_decode_impl(q, q_dtype, &out, 1, n_q, 0, out_dtype, int2_pool, int4_pool, pool_pages, pool_int4, layer,
+                           n_kv, d, n_q, batch, page_indptr, page_ids, int4_indptr, int4_ids, int4_count, work, cta_ptr,
+                           n_cta, partials, counters, scale, 0, k_new, v_new, kv_dtype, int4_pool, pool_status, flags,
+                           stream);
 }

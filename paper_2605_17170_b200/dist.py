@@ -13,6 +13,8 @@ The reference is single-process; the path shards two ways (8(e))
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -91,6 +93,83 @@ def gather_heads(out_local: torch.Tensor, out_full: torch.Tensor | None = None, 
         out_full.copy_(full)
         return out_full
     return full
+
+
+@dataclass
+class HeadOutputs:
+    """Destinations of the KV-head-parallel combine fused into the decode kernel
+    (``flash_decode_batched(..., gather=...)``, C ABI kvmix_flash_decode_gather): this rank's
+    q heads [head0, head0 + n_q_heads) are stored into each buffer ``ptrs[i]`` =
+    [B, out_heads, d] (``dtype``) -- its own and the peers' mapped over NVLink."""
+
+    ptrs: list
+    out_heads: int
+    head0: int
+    dtype: torch.dtype
+    batch: int
+    head_dim: int
+    device: torch.device | None = None
+
+    def check(self, batch: int, n_q_heads: int, head_dim: int, device) -> None:
+        if not 1 <= len(self.ptrs) <= 8:
+            raise ValidationError("the fused head gather stores to 1 to 8 buffers")
+        if any(not p for p in self.ptrs):
+            raise ValidationError("null gather destination")
+        if batch != self.batch or head_dim != self.head_dim:
+            raise ValidationError(f"gather buffers are [{self.batch}, {self.out_heads}, {self.head_dim}]")
+        if not 0 <= self.head0 or self.head0 + n_q_heads > self.out_heads:
+            raise ValidationError("this rank's head slice falls outside the gather buffers")
+        if self.device is not None and torch.device(device) != torch.device(self.device):
+            raise ValidationError(f"gather buffers live on {self.device}, the pool on {device}")
+
+    @classmethod
+    def local(cls, buffers, head0: int) -> "HeadOutputs":
+        """Destinations that are tensors of this process ([B, out_heads, d] each, contiguous)."""
+        b0 = buffers[0]
+        for b in buffers:
+            if (b.shape != b0.shape or b.dtype != b0.dtype or b.device != b0.device or not b.is_contiguous()
+                    or b.dim() != 3):
+                raise ValidationError("gather buffers must be equal contiguous [B, out_heads, d] tensors")
+        return cls([b.data_ptr() for b in buffers], b0.shape[1], head0, b0.dtype, b0.shape[0], b0.shape[2], b0.device)
+
+
+class SymmetricHeadGather:
+    """The cfg4 combine over NVLink: a symmetric-memory output [n_layers, B, Hq, d] on every
+    rank (torch.distributed._symmetric_memory: each rank's buffer is mapped into every peer's
+    address space), and per layer the HeadOutputs that make each rank's decode kernel store
+    its head slice into all ranks' buffers.  ``barrier()`` (a signal-pad barrier on the
+    device, stream-ordered) makes every rank's stores visible before the outputs are read;
+    ``gather_heads`` (NCCL all_gather_into_tensor) is the path it replaces."""
+
+    def __init__(self, n_layers: int, batch: int, n_q_heads: int, head_dim: int, dtype=torch.bfloat16,
+                 device=None, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        rank, W = world()
+        if n_q_heads % W:
+            raise ValidationError(f"{n_q_heads} q heads do not split over {W} ranks")
+        if W > 8:
+            raise ValidationError("the fused head gather spans at most 8 ranks (one NVLink domain)")
+        self.shape = (n_layers, batch, n_q_heads, head_dim)
+        self.rank, self.world, self.dtype = rank, W, dtype
+        self.head0 = rank * (n_q_heads // W)
+        self.out = symm_mem.empty(self.shape, dtype=dtype, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        self.handle = symm_mem.rendezvous(self.out, grp)
+        self._layer_bytes = batch * n_q_heads * head_dim * self.out.element_size()
+        # the tensor sits at the same offset of every rank's symmetric allocation
+        off = self.out.data_ptr() - int(self.handle.buffer_ptrs[rank])
+        self._bases = [int(self.handle.buffer_ptrs[r]) + off for r in range(W)]
+
+    def layer(self, layer: int) -> HeadOutputs:
+        L, B, Hq, d = self.shape
+        if not 0 <= layer < L:
+            raise ValidationError("layer out of range")
+        ptrs = [base + layer * self._layer_bytes for base in self._bases]
+        return HeadOutputs(ptrs, Hq, self.head0, self.dtype, B, d, self.out.device)
+
+    def barrier(self) -> None:
+        self.handle.barrier(channel=0)
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:

@@ -107,3 +107,37 @@ def test_head_shards_vs_oracle(cuda, data):
         ref = oatt.flash_decode_pool(q[i], op, f"r{i}", layer)
         err = np.abs(out[i] - ref)
         assert np.all(err <= ATOL + RTOL * np.abs(ref)), f"request {i}: max abs err {err.max():.3e}"
+
+
+@pytest.mark.parametrize("shards,dtype", [(2, torch.float32), (4, torch.bfloat16), (8, torch.float32)])
+def test_fused_head_gather(cuda, data, shards, dtype):
+    """The combine fused into the kernel (kvmix_flash_decode_gather): every shard's decode stores
+    its head slice into all destination buffers -- here three buffers of this process standing in
+    for the ranks' NVLink-mapped outputs -- and each buffer ends up equal to the unsharded decode
+    (bit for bit under the per-unit schedule, like the all-gather path)."""
+    H, Hq, d = data["H"], data["Hq"], data["d"]
+    full, rids = build(data, slice(0, H))
+    layer = 1
+    q = data["q"][layer]
+    B = len(rids)
+    ref = decode(full, rids, q, layer, n_cta=1).to(dtype)
+    dests = [torch.full((B, Hq, d), float("nan"), dtype=dtype, device="cuda") for _ in range(3)]
+    for r in range(shards):
+        kvh, qh = kvdist.head_slice(H, Hq, r, shards)
+        pool, _ = build(data, kvh)
+        b = kv.DecodeBatch(pool, rids, n_q_heads=qh.stop - qh.start, n_cta=1)
+        res = kv.flash_decode_batched(torch.as_tensor(q[:, qh], device="cuda").to(torch.bfloat16), b, layer,
+                                      gather=kvdist.HeadOutputs.local(dests, head0=qh.start))
+        assert res is None
+    for i, o in enumerate(dests):
+        assert torch.equal(o, ref), f"destination {i}: differs from the unsharded decode"
+    # out and gather together, or a head slice past the buffers, are rejected
+    with pytest.raises(kv.ValidationError):
+        kv.flash_decode_batched(torch.as_tensor(q, device="cuda").to(torch.bfloat16), kv.DecodeBatch(full, rids, n_q_heads=Hq),
+                                layer, out=dests[0], gather=kvdist.HeadOutputs.local(dests, head0=0))
+    with pytest.raises(kv.ValidationError):
+        kvh, qh = kvdist.head_slice(H, Hq, shards - 1, shards)
+        pool, _ = build(data, kvh)
+        kv.flash_decode_batched(torch.as_tensor(q[:, qh], device="cuda").to(torch.bfloat16),
+                                kv.DecodeBatch(pool, rids, n_q_heads=qh.stop - qh.start), layer,
+                                gather=kvdist.HeadOutputs.local(dests, head0=qh.start + 1))

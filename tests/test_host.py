@@ -7,6 +7,7 @@ import re
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2605_17170_b200 as kv
 from paper_2605_17170_b200 import _lib
@@ -75,6 +76,32 @@ def test_abi_validation_without_gpu():
                                      None, None, None, 3, None, None, 1.0, 0, None, 0, None)
     with pytest.raises(kv.ValidationError, match="multiple"):
         _lib.check(rc)
+
+
+def test_gather_validation_without_gpu():
+    """The fused head gather (kvmix_flash_decode_gather) rejects bad destinations before any
+    CUDA call; HeadOutputs checks the same on the host."""
+    import ctypes
+
+    from paper_2605_17170_b200 import dist as kvdist
+
+    fake = 16  # never dereferenced: validation returns first
+    def call(n_outs, out_heads, head0, null=False):
+        ptrs = (ctypes.c_void_p * 9)(*([None] if null else []) + [fake] * (9 - int(null)))
+        return _lib.lib.kvmix_flash_decode_gather(
+            fake, 1, ctypes.cast(ptrs, ctypes.c_void_p), n_outs, out_heads, head0, 1, fake, fake, 1, 1, 0, 1, 128, 8,
+            1, fake, fake, fake, fake, None, fake, fake, 1, fake, fake, 1.0, 0, None, 0, None)
+    for args, msg in [((9, 8, 0), "output buffers"), ((0, 8, 0), "output buffers"), ((2, 8, 1), "head slice"),
+                      ((2, 16, -1), "head slice"), ((2, 16, 0, True), "null")]:
+        with pytest.raises(kv.ValidationError, match=msg):
+            _lib.check(call(*args))
+    ho = kvdist.HeadOutputs([fake, fake], out_heads=16, head0=8, dtype=torch.bfloat16, batch=2, head_dim=128)
+    ho.check(2, 8, 128, "cpu")
+    for bad in [(2, 16, 128), (3, 8, 128), (2, 8, 64)]:
+        with pytest.raises(kv.ValidationError):
+            ho.check(*bad, "cpu")
+    with pytest.raises(kv.ValidationError):
+        kvdist.HeadOutputs([fake] * 9, 16, 0, torch.bfloat16, 2, 128).check(2, 8, 128, "cpu")
 
 
 # ---- control plane vs the oracle and the reference trace --------------------------------------
