@@ -300,7 +300,7 @@ struct PrefillCfg {
   static constexpr int SWZ = CHUNKS >= 8 ? 7 : CHUNKS - 1;
   static constexpr int TILE = G * ROWB;
   static constexpr int STAGES = KVMIX_K1_STAGES;  // 2 or 3 items of K / V rows in flight per CTA
-  static constexpr int SMEM = 2 * STAGES * TILE + page_stride(D);  // stages x (K, V) + the record
+  static constexpr int SMEM = 2 * STAGES * TILE + page_stride(D) + 16;  // stages x (K, V) + the record + page ids
 };
 
 template <int D, typename T>
@@ -343,26 +343,39 @@ __device__ __forceinline__ void load_pair(uint8_t* tile, int row, int c, float& 
   }
 }
 
-// Item cursor for the persistent page CTAs: item = lh * n_pages + p, lh = l * H + h,
-// advanced by the grid stride with precomputed carries (no 64-bit division per item).
+// Item cursor for the persistent page CTAs, advanced by the grid stride with precomputed
+// carries (no 64-bit division per item).  KVMIX_K1_ORDER 1 (default): item = (l * n_pages + p)
+// * H + h -- the CTAs resident at one time cover all kv heads of a run of pages, so the rows
+// they gather (256 B per head of a 2 KB token row [H][d]) complete whole token rows together
+// (DRAM page locality); 0: item = (l * H + h) * n_pages + p (one head's pages at a time).
+#ifndef KVMIX_K1_ORDER
+#define KVMIX_K1_ORDER 1
+#endif
 struct ItemCursor {
-  int p, h, l;
-  __device__ void init(int64_t item, int np, int H) {
-    const int64_t lh = item / np;
-    p = (int)(item - lh * np);
-    l = (int)(lh / H);
-    h = (int)(lh - (int64_t)l * H);
+  int a, b, l;  // inner / middle / outer coordinate
+#if KVMIX_K1_ORDER
+  __device__ __forceinline__ int page() const { return b; }
+  __device__ __forceinline__ int head() const { return a; }
+#else
+  __device__ __forceinline__ int page() const { return a; }
+  __device__ __forceinline__ int head() const { return b; }
+#endif
+  __device__ void init(int64_t item, int na, int nb) {
+    const int64_t ab = item / na;
+    a = (int)(item - ab * na);
+    l = (int)(ab / nb);
+    b = (int)(ab - (int64_t)l * nb);
   }
-  __device__ void advance(int dp, int dh, int dl, int np, int H) {
-    p += dp;
-    h += dh;
+  __device__ void advance(int da, int db, int dl, int na, int nb) {
+    a += da;
+    b += db;
     l += dl;
-    if (p >= np) {
-      p -= np;
-      ++h;
+    if (a >= na) {
+      a -= na;
+      ++b;
     }
-    if (h >= H) {
-      h -= H;
+    if (b >= nb) {
+      b -= nb;
       ++l;
     }
   }
@@ -393,28 +406,39 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
   const int ch = tid % P::CHUNKS, r0 = tid / P::CHUNKS;
   const int np = (int)n_pages, H = (int)n_kv_heads;
   const int64_t grid = gridDim.x;
-  const int dp = (int)(grid % np), dlh = (int)(grid / np);
-  const int dh = dlh % H, dl = dlh / H;
+#if KVMIX_K1_ORDER
+  const int na = H, nb = np;
+#else
+  const int na = np, nb = H;
+#endif
+  const int da = (int)(grid % na);
+  const int64_t dab = grid / na;
+  const int db = (int)(dab % nb), dl = (int)(dab / nb);
   // cursors of this item and the next three: with 2 stages nxt is fetched while this one is
   // encoded and nn's indices load; with 3 stages nn is fetched and n3's indices load
   ItemCursor cur, nxt, nn, n3;
-  cur.init(blockIdx.x, np, H);
+  cur.init(blockIdx.x, na, nb);
   nxt = cur;
-  nxt.advance(dp, dh, dl, np, H);
+  nxt.advance(da, db, dl, na, nb);
   nn = nxt;
-  nn.advance(dp, dh, dl, np, H);
+  nn.advance(da, db, dl, na, nb);
   n3 = nn;
-  n3.advance(dp, dh, dl, np, H);
-  int tok_a[NPASS], tok_b[NPASS], pid_n = 0, pid_nn = 0, pid_n3 = 0;  // indices loaded ahead
-  auto load_tok = [&](const ItemCursor& c, int64_t item, int (&tok)[NPASS], int& pid) {
+  n3.advance(da, db, dl, na, nb);
+  // Token ids are loaded into registers two items ahead.  The page id travels with the item's
+  // tiles (one 4 B cp.async by thread 0 into spid[stage]): kept in a register it is CTA-uniform,
+  // and the compiler moved it into a uniform register right at its load -- a full load-latency
+  // stall per item (19% of the kernel's stall samples in ncu).
+  int* spid = reinterpret_cast<int*>(srec + page_stride(D));
+  int tok_a[NPASS], tok_b[NPASS];
+  auto load_tok = [&](const ItemCursor& c, int64_t item, int (&tok)[NPASS]) {
 #pragma unroll
-    for (int j = 0; j < NPASS; ++j) tok[j] = item < n_items ? __ldg(page_tokens + (int64_t)c.p * G + r0 + RPP * j) : 0;
-    pid = item < n_items ? __ldg(page_ids + c.p) : 0;
+    for (int j = 0; j < NPASS; ++j) tok[j] = item < n_items ? __ldg(page_tokens + (int64_t)c.page() * G + r0 + RPP * j) : 0;
   };
   const int64_t row_step = (int64_t)H * D;  // elements between consecutive tokens
   auto fetch = [&](const ItemCursor& c, const int (&tok)[NPASS], int stg) {
     uint8_t* Ks = psm + 2 * stg * P::TILE;
-    const int64_t base = ((int64_t)c.l * n_tokens * H + c.h) * D;
+    if (tid == 0) cp_async4(spid + stg, page_ids + c.page());
+    const int64_t base = ((int64_t)c.l * n_tokens * H + c.head()) * D;
 #pragma unroll
     for (int j = 0; j < NPASS; ++j) {
       const int r = r0 + RPP * j;
@@ -424,30 +448,30 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
       cp_async16(dst + P::TILE, reinterpret_cast<const uint8_t*>(values + off) + 16 * ch);
     }
   };
-  int stg = 0, pid = 0;
+  int stg = 0;
   float kmx = 0.f, vmx = 0.f;  // largest key-page / V scales this thread stored (pool status)
   {
     int tok0[NPASS];
-    load_tok(cur, blockIdx.x, tok0, pid);
+    load_tok(cur, blockIdx.x, tok0);
     if (blockIdx.x < n_items) fetch(cur, tok0, 0);
     cp_async_commit();
     if constexpr (P::STAGES == 3) {
-      load_tok(nxt, blockIdx.x + grid, tok0, pid_n);
+      load_tok(nxt, blockIdx.x + grid, tok0);
       if (blockIdx.x + grid < n_items) fetch(nxt, tok0, 1);
       cp_async_commit();
-      load_tok(nn, blockIdx.x + 2 * grid, tok_a, pid_nn);
+      load_tok(nn, blockIdx.x + 2 * grid, tok_a);
     } else {
-      load_tok(nxt, blockIdx.x + grid, tok_a, pid_n);
+      load_tok(nxt, blockIdx.x + grid, tok_a);
     }
   }
   for (int64_t item = blockIdx.x; item < n_items; item += grid, stg = stg + 1 == P::STAGES ? 0 : stg + 1) {
     if constexpr (P::STAGES == 3) {
-      load_tok(n3, item + 3 * grid, tok_b, pid_n3);
+      load_tok(n3, item + 3 * grid, tok_b);
       if (item + 2 * grid < n_items) fetch(nn, tok_a, stg == 0 ? 2 : stg - 1);
       cp_async_commit();
       cp_async_wait<2>();  // this item's tiles have landed (the next two may still fly)
     } else {
-      load_tok(nn, item + 2 * grid, tok_b, pid_nn);
+      load_tok(nn, item + 2 * grid, tok_b);
       if (item + grid < n_items) fetch(nxt, tok_a, stg ^ 1);
       cp_async_commit();
       cp_async_wait<1>();  // this item's tiles have landed (the next item's may still fly)
@@ -503,18 +527,16 @@ __global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict_
     fence_proxy_async_smem();  // each thread's record writes, ordered before the bulk store's reads
     __syncthreads();
     if (tid == 0) {  // the record leaves with one TMA bulk store; srec is reused after it was read
-      bulk_s2g(int2_pool + (((int64_t)cur.l * H + cur.h) * pool_pages + pid) * page_stride(D), srec, page_stride(D));
+      const int pid = spid[stg];  // landed with this stage's tiles
+      bulk_s2g(int2_pool + (((int64_t)cur.l * H + cur.head()) * pool_pages + pid) * page_stride(D), srec, page_stride(D));
       bulk_commit();
     }
     cur = nxt;
     nxt = nn;
     nn = n3;
-    n3.advance(dp, dh, dl, np, H);
+    n3.advance(da, db, dl, na, nb);
 #pragma unroll
     for (int j = 0; j < NPASS; ++j) tok_a[j] = tok_b[j];
-    pid = pid_n;
-    pid_n = pid_nn;
-    pid_nn = pid_n3;
   }
   cp_async_wait<0>();
   if (tid == 0) bulk_wait_read0();
@@ -558,8 +580,15 @@ __global__ void __launch_bounds__(128, KVMIX_INT4_MINB) int4_tokens_kernel(const
   constexpr int SS = slot_stride(D), NG = D / 32, TPW = 32 / NG;  // tokens per warp
   __shared__ __align__(16) uint8_t srec[4][TPW * SS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x / 32;
+  // grid (chunks * H, 1, L): the kv head is the fastest index (KVMIX_K1_ORDER), so the CTAs
+  // resident together read whole 2 KB token rows [H][d]
+#if KVMIX_K1_ORDER
+  const int h = (int)(blockIdx.x % (unsigned)n_kv_heads), l = blockIdx.z;
+  const int64_t i0 = ((int64_t)(blockIdx.x / (unsigned)n_kv_heads) * 4 + warp) * TPW;  // first token of this warp
+#else
   const int h = blockIdx.y, l = blockIdx.z;
-  const int64_t i0 = ((int64_t)blockIdx.x * 4 + warp) * TPW;  // first token index of this warp
+  const int64_t i0 = ((int64_t)blockIdx.x * 4 + warp) * TPW;
+#endif
   if (i0 >= n) return;
   uint8_t* st = srec[warp];
   for (int k = lane; k < TPW * SS / 4; k += 32) reinterpret_cast<uint32_t*>(st)[k] = 0u;  // padding stays zero
@@ -832,7 +861,11 @@ static int launch_prefill(const void* keys, const void* values, int64_t L, int64
   }
   if (n4 > 0) {
     const int64_t tpc = 4 * (32 / (d / 32));  // tokens per CTA
+#if KVMIX_K1_ORDER
+    dim3 grid((unsigned)((n4 + tpc - 1) / tpc * H), 1, (unsigned)L);
+#else
     dim3 grid((unsigned)((n4 + tpc - 1) / tpc), (unsigned)H, (unsigned)L);
+#endif
     DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>(k, v, n4, N * H * D, H * D, H, 0, int4_tokens,
                                                                 int4_ids, int4_pool, pool_int4, err));
   }
@@ -866,7 +899,11 @@ static int launch_append(const void* k, const void* v, int64_t n, int64_t Lin, i
                          int64_t layer_stride, int64_t tok_stride, const int32_t* int4_ids, uint8_t* int4_pool,
                          int64_t pool_int4, int32_t* err, cudaStream_t s) {
   const int64_t tpc = 4 * (32 / (d / 32));  // tokens per CTA
+#if KVMIX_K1_ORDER
+  dim3 grid((unsigned)((n + tpc - 1) / tpc * H), 1, (unsigned)Lin);
+#else
   dim3 grid((unsigned)((n + tpc - 1) / tpc), (unsigned)H, (unsigned)Lin);
+#endif
   DISPATCH_D(d, int4_tokens_kernel<D, T><<<grid, 128, 0, s>>>((const T*)k, (const T*)v, n, layer_stride, tok_stride, H,
                                                               layer0, nullptr, int4_ids, int4_pool, pool_int4, err));
   return check_launch("append_int4");
