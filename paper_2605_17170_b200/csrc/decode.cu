@@ -57,6 +57,9 @@ constexpr float RESCALE_SLACK = 8.f;  // largest lazy-rescale slack (log2 units)
 #ifndef KVMIX_Q2EXACT
 #define KVMIX_Q2EXACT 1  // INT2 key pages: q*s as an exact fp16 hi + lo pair (two MMAs per chunk)
 #endif
+#ifndef KVMIX_KZBATCH
+#define KVMIX_KZBATCH 1  // INT2 key bias sum_c q_c z_c for 16 pages per NCH MMAs (0: NCH MMAs per page)
+#endif
 #ifndef KVMIX_Q2ACC
 #define KVMIX_Q2ACC 1  // 1: the lo MMAs accumulate into the hi accumulators (fewer registers, longer chains)
 #endif
@@ -77,9 +80,14 @@ struct Cfg {
   // piece's first copies then start after the merge instead of during it.
   static constexpr bool MERGE_IN_RING = KVMIX_MINB >= 4;
   static_assert(!MERGE_IN_RING || MERGE <= NW * STAGES * BUF, "merge scratch must fit in the ring");
+  // batched key bias: per warp, the KZ regions (2D bytes) of its next 16 INT2 pages; they live
+  // in the merge scratch (idle during the tile loop) unless the merge itself lives in the ring
+  static constexpr int KZB = 2 * D;
+  static constexpr int KZS = KVMIX_KZBATCH ? NW * 16 * KZB : 0;
+  static constexpr bool KZ_IN_MERGE = !MERGE_IN_RING && KZS <= MERGE;
   static constexpr int QS = D + 4;                                // raw q row stride (floats; 4-way LDS conflicts at most)
   static constexpr int QRAW = 8 * QS * 4;                          // the unit's raw q [8 heads][D] (fp32) for build_qtab
-  static constexpr int SMEM = NW * STAGES * BUF + QTAB + (MERGE_IN_RING ? 0 : MERGE) + QRAW;
+  static constexpr int SMEM = NW * STAGES * BUF + QTAB + (MERGE_IN_RING ? 0 : MERGE) + QRAW + (KZ_IN_MERGE ? 0 : KZS);
 };
 
 constexpr int MAX_OUTS = 8;  // destinations of the fused head all-gather (one NVLink domain)
@@ -464,7 +472,7 @@ struct QFrag {
 // tokens T0 = 8q + 2ks, T1 = T0 + 4 (a0) and T0+1, T1+1 (a2).
 template <int D, bool LO>
 __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
-                                        int lane, const Softmax& st, float (&sv)[8]) {
+                                        int lane, const Softmax& st, float (&sv)[8], float kb0, float kb1) {
   using C = Cfg<D>;
   constexpr int KB = D / 4, LB = KB < 16 ? KB : 16;
   const int g = lane >> 2, q = lane & 3;
@@ -496,7 +504,7 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
     const int P4 = 0, odd = i & 1;
     if (!odd) {
       lds_vec<16>(buf + PG_KS(D) + (4 * (i >> 1) + q) * 16, ksw);
-      lds_vec<16>(buf + PG_KZ(D) + (4 * (i >> 1) + q) * 16, kzw);
+      if (!KVMIX_KZBATCH) lds_vec<16>(buf + PG_KZ(D) + (4 * (i >> 1) + q) * 16, kzw);
     }
 #else
     const int P4 = 4 * (i >> 1), odd = i & 1;
@@ -548,8 +556,14 @@ __device__ __forceinline__ void int2_qk(const uint8_t* __restrict__ buf, const Q
     mma16816_b64(d1, a10, a11, a12, a13, qr);
 #endif
 #endif
-    mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qi);
-    if constexpr (LO) mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qf.b2lo(i));
+    if (!KVMIX_KZBATCH) {
+      mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qi);
+      if constexpr (LO) mma16816_b64(odd ? cbO : cbE, kzw[P4], kzw[P4 + 1], kzw[P4 + 2], kzw[P4 + 3], qf.b2lo(i));
+    }
+  }
+  if (KVMIX_KZBATCH) {  // the page's bias, computed for its batch of 16 pages (int2_batch_bias)
+    cbE[0] = kb0;
+    cbE[1] = kb1;
   }
   const float b0 = fmaf(cbE[0] + cbO[2], qscale, -st.m0), b1 = fmaf(cbE[1] + cbO[3], qscale, -st.m1);
   const float f0 = KF0 * qscale, f1 = KF1 * qscale, f2 = KF2 * qscale, f3 = KF3 * qscale;
@@ -592,12 +606,36 @@ __device__ __forceinline__ void int2_pv(const uint8_t* __restrict__ buf, const u
   }
 }
 
+// Key bias sum_c q_c z_c of 16 INT2 pages at once (KVMIX_KZBATCH): A rows g / g+8 = the zero
+// points of pages g / g+8 of the batch (their KZ regions, staged in kzs), B = the chunk's q
+// fragment, so NCH MMAs cover 16 pages instead of NCH per page.  d[0..1] = page g's bias for
+// heads 2q, 2q+1, d[2..3] = page g+8's.
+template <int D, bool LO>
+__device__ __forceinline__ void int2_batch_bias(const uint8_t* __restrict__ kzs, const QFrag<D, LO>& qf, int lane,
+                                                float (&d)[4]) {
+  using C = Cfg<D>;
+  const int g = lane >> 2, q = lane & 3;
+  d[0] = d[1] = d[2] = d[3] = 0.f;
+#pragma unroll
+  for (int P = 0; P < C::NCH / 2; ++P) {
+    uint32_t wa[4], wb[4];  // quad (z_2P.p0, z_2P+1.p0, z_2P.p1, z_2P+1.p1) of pages g and g+8
+    lds_vec<16>(kzs + g * C::KZB + (4 * P + q) * 16, wa);
+    lds_vec<16>(kzs + (g + 8) * C::KZB + (4 * P + q) * 16, wb);
+    mma16816_b64(d, wa[0], wb[0], wa[2], wb[2], qf.b2(2 * P));
+    mma16816_b64(d, wa[1], wb[1], wa[3], wb[3], qf.b2(2 * P + 1));
+    if constexpr (LO) {
+      mma16816_b64(d, wa[0], wb[0], wa[2], wb[2], qf.b2lo(2 * P));
+      mma16816_b64(d, wa[1], wb[1], wa[3], wb[3], qf.b2lo(2 * P + 1));
+    }
+  }
+}
+
 template <int D, bool LO>
 __device__ __forceinline__ void int2_tile(const uint8_t* __restrict__ buf, const QFrag<D, LO>& qf, float qscale,
-                                          int lane, Softmax& st, Acc<D>& acc) {
+                                          int lane, Softmax& st, Acc<D>& acc, float kb0 = 0.f, float kb1 = 0.f) {
   float sv[8];
   uint32_t bP[2][2];
-  int2_qk<D, LO>(buf, qf, qscale, lane, st, sv);
+  int2_qk<D, LO>(buf, qf, qscale, lane, st, sv, kb0, kb1);
   softmax_tile<D>(sv, st, acc, bP);
   int2_pv<D>(buf, bP, lane, acc);
 }
@@ -971,6 +1009,7 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   using C = Cfg<D>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[NW][STAGES];
+  __shared__ __align__(8) uint64_t kzbar[NW];  // this warp's KZ batch copies
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   uint8_t* ring = smem + warp * STAGES * C::BUF;
@@ -980,12 +1019,16 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[warp][s], 1);
+    mbar_init(&kzbar[warp], 1);
     fence_mbar_init();
   }
   __syncwarp();
   pdl_launch_dependents();  // the next kernel may start prefetching its KV tiles
   int stage = 0;  // ring position and mbarrier phase persist across pieces
   uint32_t phase = 0;
+  uint32_t kzphase = 0;
+  uint8_t* kzs = (C::KZ_IN_MERGE ? smem + NW * STAGES * C::BUF + C::QTAB
+                                 : smem + C::SMEM - C::KZS) + warp * 16 * C::KZB;
   bool waited = false;  // q, out, partials and counters are touched only after pdl_wait()
 
   if (a.flags & KVMIX_DECODE_POOL_WRITTEN) {  // the previous kernel wrote the pool: no early KV copies
@@ -1028,6 +1071,23 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
   }
   primed = false;
   int meta_next = load_meta(STAGES), meta_next2 = load_meta(STAGES + 1);  // metas run two tiles ahead
+  // batched key bias: this warp's INT2 tiles are its first k2 tiles; batch b = tiles 16b..16b+15,
+  // whose KZ regions one bulk copy per lane stages into kzs (issued one batch ahead)
+  const int t0w = u.tlo + warp;
+  const int k2 = (KVMIX_KZBATCH && t0w < u.npg) ? min(nmine, (u.npg - t0w + NW - 1) / NW) : 0;
+  auto issue_kz = [&](int b) {
+    const int n = min(16, k2 - 16 * b);
+    __syncwarp();
+    fence_proxy_async();  // the slots were last accessed through the generic proxy
+    if (lane == 0) mbar_expect_tx(&kzbar[warp], n * C::KZB);
+    __syncwarp();
+    if (lane < n) {
+      const int pid = a.page_ids[u.pg0 + t0w + (16 * b + lane) * NW];
+      bulk_g2s(kzs + lane * C::KZB, kv2 + (int64_t)pid * C::PS + PG_KZ(D), C::KZB, &kzbar[warp]);
+    }
+  };
+  if (MEMORY && k2 > 0) issue_kz(0);
+  float kbd[4] = {0.f, 0.f, 0.f, 0.f};  // the current batch's biases (int2_batch_bias)
 
   // ---- Q fragments (see QFrag): built once per CTA by warp 0 into shared memory ----
   // The KV tiles above are this launch's own inputs (written by earlier steps); q, out and
@@ -1084,7 +1144,20 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
     if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
     } else if (t < u.npg) {
-      int2_tile<D, LO>(buf, qf, qscale, lane, st, acc);
+      float kb0 = 0.f, kb1 = 0.f;
+      if (KVMIX_KZBATCH) {
+        const int j = k & 15;
+        if (j == 0) {
+          if (MEMORY) mbar_wait(&kzbar[warp], kzphase);
+          kzphase ^= 1u;
+          int2_batch_bias<D, LO>(kzs, qf, lane, kbd);
+          if (MEMORY && k + 16 < k2) issue_kz(k / 16 + 1);
+        }
+        const int src = 4 * (j & 7) + q;
+        kb0 = __shfl_sync(0xffffffffu, j < 8 ? kbd[0] : kbd[2], src);
+        kb1 = __shfl_sync(0xffffffffu, j < 8 ? kbd[1] : kbd[3], src);
+      }
+      int2_tile<D, LO>(buf, qf, qscale, lane, st, acc, kb0, kb1);
     } else {
       const int nv = min(32, u.n4 - 32 * (t - u.npg));
       if (nv == 32) int4_tile<D, true, LO>(buf, 32, qf, qscale, lane, st, acc);

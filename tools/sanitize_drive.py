@@ -31,11 +31,11 @@ ATOL, RTOL = 2e-3, 1e-2
 def main():
     rng = np.random.default_rng(7)
     L, H, Hq, d = 2, 2, 16, 128
-    total, offset = 6000, 3200
+    total, offset = 14000, 9600
     pool = kv.MixedPrecisionPool(kv.PoolConfig(total_slots=total, offset=offset, n_layers=L, n_kv_heads=H, head_dim=d))
     op = opool.OraclePool(opool.Config(total, offset, L, H, d))
     rids = []
-    for r, n in enumerate([37, 300, 1100]):
+    for r, n in enumerate([37, 300, 1100, 6000]):
         bits = np.where(rng.random(n) < 0.8, 2, 4)
         k = torch.randn(L, n, H, d).to(torch.bfloat16).float().numpy()
         v = torch.randn(L, n, H, d).to(torch.bfloat16).float().numpy()
@@ -57,7 +57,7 @@ def main():
     kv.encode_token_blocks(rng.standard_normal((5, d)).astype(np.float32), 2)
 
     q = torch.randn(len(rids), Hq, d).to(torch.bfloat16)
-    for n_cta in (3, 37):  # split units: partial slots + last-arriver combine
+    for n_cta in (1, 3, 37):  # 1: long single pieces (several key-bias batches per warp); split units: partial slots + last-arriver combine
         b = kv.DecodeBatch(pool, rids, n_q_heads=Hq, n_cta=n_cta)
         for layer in range(L):
             out = kv.flash_decode_batched(q.cuda(), b, layer, out=torch.empty(q.shape, device="cuda"))
