@@ -798,9 +798,11 @@ __device__ __forceinline__ void issue_tile(const Unit& u, int t, int meta, uint8
                                            const uint8_t* kv2, const uint8_t* kv4) {
   using C = Cfg<D>;
   if (t < u.npg) {
+    // with the batched key bias the record's trailing key zeros stay out of the tile copy
+    constexpr int NB = KVMIX_KZBATCH ? PG_KZ(D) : C::PS;
     if (lane == 0) {
-      mbar_expect_tx(bar, C::PS);
-      bulk_g2s(buf, kv2 + (int64_t)meta * C::PS, C::PS, bar);
+      mbar_expect_tx(bar, NB);
+      bulk_g2s(buf, kv2 + (int64_t)meta * C::PS, NB, bar);
     }
   } else {
     const int nv = min(32, u.n4 - 32 * (t - u.npg));

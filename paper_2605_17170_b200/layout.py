@@ -21,12 +21,13 @@ plus the page's 32 INT2 V TokenBlocks (quant.py:145-262) in slot order::
   KS [8d, 10d)   key scales, fp16: lane q owns channels [q d/4, (q+1) d/4) in 8-channel chunks;
                  chunk i of lane q is chunk 4i + q; channel 8P + 4I + e of a chunk sits
                  at 4(e>>1) + 2I + (e&1)
-  KZ [10d, 12d)  key zeros, same order
-  VC [12d, 20d)  value codes: word ((ks*8 + g)*4 + q)*ng + j holds code byte
+  VC [10d, 18d)  value codes: word ((ks*8 + g)*4 + q)*ng + j holds code byte
                  b = 8j + g of tokens [T0, T0+1, T1, T1+1], T0 = 8q + 2ks, T1 = T0 + 4
-  VS [20d, 22d)  value scales: half (((j*4 + q)*2 + p)*2 + ks)*2 + h is the scale of
+  VS [18d, 20d)  value scales: half (((j*4 + q)*2 + p)*2 + ks)*2 + h is the scale of
                  group j of token 8q + 2ks + 4h + p
-  VZ [22d, 24d)  value zeros, same order
+  VZ [20d, 22d)  value zeros, same order
+  KZ [22d, 24d)  key zeros, in the KS order (last: the decode kernel copies [0, 22d) per
+                 tile and stages the zeros of 16 pages at once for its batched key bias)
 
 INT4 slot record (d + 8 ng bytes, rounded up to 16; 160 at d = 128) = INT4 K
 TokenBlock then INT4 V TokenBlock, each permuted as::
@@ -76,7 +77,7 @@ def page_perm(d: int) -> np.ndarray:
         pos = _kp_pos(d, c)
         for k in range(2):
             perm[8 * d + 2 * pos + k] = 8 * d + 4 * c + k  # scale_c
-            perm[10 * d + 2 * pos + k] = 8 * d + 4 * c + 2 + k  # zero_c
+            perm[22 * d + 2 * pos + k] = 8 * d + 4 * c + 2 + k  # zero_c
     for ks in range(2):
         for g in range(8):
             for q in range(4):
@@ -84,7 +85,7 @@ def page_perm(d: int) -> np.ndarray:
                     w = ((ks * 8 + g) * 4 + q) * ng + j
                     t0 = 8 * q + 2 * ks
                     for pos, t in enumerate((t0, t0 + 1, t0 + 4, t0 + 5)):
-                        perm[12 * d + 4 * w + pos] = kp + t * tb2 + 8 * j + g
+                        perm[10 * d + 4 * w + pos] = kp + t * tb2 + 8 * j + g
     for ks in range(2):
         for q in range(4):
             for j in range(ng):
@@ -93,8 +94,8 @@ def page_perm(d: int) -> np.ndarray:
                         idx = (((j * 4 + q) * 2 + p) * 2 + ks) * 2 + h
                         t = 8 * q + 2 * ks + 4 * h + p
                         for k in range(2):
-                            perm[20 * d + 2 * idx + k] = kp + t * tb2 + d // 4 + 4 * j + k
-                            perm[22 * d + 2 * idx + k] = kp + t * tb2 + d // 4 + 4 * j + 2 + k
+                            perm[18 * d + 2 * idx + k] = kp + t * tb2 + d // 4 + 4 * j + k
+                            perm[20 * d + 2 * idx + k] = kp + t * tb2 + d // 4 + 4 * j + 2 + k
     assert (np.sort(perm) == np.arange(page_stride(d))).all()
     return perm
 
