@@ -141,3 +141,34 @@ def test_fused_head_gather(cuda, data, shards, dtype):
         kv.flash_decode_batched(torch.as_tensor(q[:, qh], device="cuda").to(torch.bfloat16),
                                 kv.DecodeBatch(pool, rids, n_q_heads=qh.stop - qh.start), layer,
                                 gather=kvdist.HeadOutputs.local(dests, head0=qh.start + 1))
+
+
+def test_symmetric_head_gather_one_rank(cuda, data):
+    """The multi-rank combine's real plumbing on a one-rank NCCL group: symmetric-memory
+    allocation and rendezvous, the per-layer destination pointers, the fused-gather decode into
+    them and the device barrier; the symmetric output equals the plain decode bit for bit."""
+    import socket
+
+    import torch.distributed as dist
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        H, Hq, d, L = data["H"], data["Hq"], data["d"], data["L"]
+        full, rids = build(data, slice(0, H))
+        sg = kvdist.SymmetricHeadGather(L, len(rids), Hq, d, dtype=torch.bfloat16, device="cuda")
+        b = kv.DecodeBatch(full, rids, n_q_heads=Hq)
+        for layer in range(L):
+            q = torch.as_tensor(data["q"][layer], device="cuda").to(torch.bfloat16)
+            assert kv.flash_decode_batched(q, b, layer, gather=sg.layer(layer)) is None
+        sg.barrier()
+        torch.cuda.synchronize()
+        for layer in range(L):
+            q = torch.as_tensor(data["q"][layer], device="cuda").to(torch.bfloat16)
+            ref = kv.flash_decode_batched(q, b, layer, out=torch.empty(q.shape, dtype=torch.bfloat16, device="cuda"))
+            assert torch.equal(sg.out[layer], ref), f"layer {layer}"
+    finally:
+        dist.destroy_process_group()
