@@ -812,16 +812,24 @@ def run_heads(args, world, rank, local, device):
     for _ in range(max(args.warmup, 1)):
         step()
     g_attn = capture(attn)
-    ms_attn = timer(g_attn.replay, args.steps)
     if world > 1 and fused:
-        ms_step = timer(step, args.steps)  # eager: the symmetric-memory barrier stays outside a graph
+        step_fn = step  # eager: the symmetric-memory barrier stays outside a graph
     elif world > 1 or fused:
         g_step = capture(step)
         for _ in range(2):
             g_step.replay()
-        ms_step = timer(g_step.replay, args.steps)
+        step_fn = g_step.replay
     else:
-        ms_step = ms_attn
+        step_fn = None
+    # attention-only and full steps timed alternately (3 rounds, medians): long cfg4 shards run
+    # into the power cap, which a back-to-back pair would charge to whichever ran second
+    t_attn, t_step = [], []
+    for _ in range(3):
+        t_attn.append(timer(g_attn.replay, args.steps))
+        if step_fn is not None:
+            t_step.append(timer(step_fn, args.steps))
+    ms_attn = float(np.median(t_attn))
+    ms_step = float(np.median(t_step)) if t_step else ms_attn
     if fused and world == 1:  # the shard's slice landed in the full-size output, equal to the plain decode's
         torch.cuda.synchronize()
         attn()
