@@ -179,6 +179,26 @@ def test_batched_mixed_lengths_and_dtypes(cuda):
                 assert ok, (layer, qd, od, r, err)
 
 
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_long_pieces_every_head_dim(cuda, d):
+    """Long single pieces at every head dim: each warp runs several batches of 16 INT2 pages
+    through the batched key bias (the zero points staged one batch ahead into the merge
+    scratch), for fp32, bf16 and f16 q, under the one-CTA schedule and the stream-K default."""
+    n, n_kv, H = 9000, 2, 8
+    pool, t, op, *_ = build(900 + d, n, n_kv, d, 0.85)
+    batch_one = kv.DecodeBatch(pool, ["req"], n_q_heads=H, n_cta=1)
+    batch_sk = kv.DecodeBatch(pool, ["req"], n_q_heads=H)
+    rng = np.random.default_rng(d)
+    q = torch.as_tensor(rng.standard_normal((1, H, d)).astype(np.float32), device=cuda)
+    for qd in (torch.float32, torch.bfloat16, torch.float16):
+        qq = q.to(qd)
+        ref = oatt.flash_decode_pool(qq[0].float().cpu().numpy(), op, "req", 0)
+        for b in (batch_one, batch_sk):
+            out = kv.flash_decode_batched(qq, b, 0, out=torch.empty(1, H, d, device=cuda))
+            ok, err = close(out[0].cpu().numpy(), ref)
+            assert ok, (d, qd, b.n_cta, err)
+
+
 def test_decode_after_append(cuda):
     pool, t, op, *_ = build(5, 700, 2, 128, 0.8, L=2, headroom=128)
     rng = np.random.default_rng(1)
