@@ -448,12 +448,12 @@ constexpr float KF4 = P20;
 //         (round 1's subnormal / normal-code forms paired (cb, cb+2) / (cb+1, cb+3))
 //  b4[2j], b4[2j+1]  INT4 keys, group j, lane q: cb = 32j + 8q: (cb+1, cb+5) / (cb, cb+4) and
 //         (cb+2, cb+6) / (cb+3, cb+7)
-//  qz     (Q_2q, Q_2q+1) / 0 with Q_j = sum of q over channel group j (hi and lo fp16 parts)
+//  qz     (Q_2q, Q_2q+1) hi / lo fp16 parts (k-lo / k-hi), Q_j = sum of q over channel group j
 // With LO (fp32 q) the *lo arrays hold q - fp16(q).
 template <int D, bool LO>
 struct QFrag {
   static constexpr int NCH = D / 16;
-  // fragment index f: b2 [0, NCH), b4 [NCH, 2NCH), qz 2NCH, qzlo 2NCH+1, b2lo / b4lo after
+  // fragment index f: b2 [0, NCH), b4 [NCH, 2NCH), qz 2NCH (2NCH+1 unused), b2lo / b4lo after
   static constexpr int F = 2 * NCH + 2 + (LO ? 2 * NCH : 0);
   static constexpr int BYTES = F * 32 * 8;
   const uint64_t* p;  // this lane's column of the CTA's [F][32 lanes] fragment table in smem
@@ -461,7 +461,6 @@ struct QFrag {
   __device__ __forceinline__ uint64_t b2(int i) const { return at(i); }
   __device__ __forceinline__ uint64_t b4(int i) const { return at(NCH + i); }
   __device__ __forceinline__ uint64_t qz() const { return at(2 * NCH); }
-  __device__ __forceinline__ uint64_t qzlo() const { return at(2 * NCH + 1); }
   __device__ __forceinline__ uint64_t b2lo(int i) const { return at(2 * NCH + 2 + i); }
   __device__ __forceinline__ uint64_t b4lo(int i) const { return at(3 * NCH + 2 + i); }
 };
@@ -688,8 +687,8 @@ __device__ __forceinline__ void int4_qk(const uint8_t* __restrict__ buf, int nv,
       if (q == 0) { za = pa[0] >> 16; zb = pb[0] >> 16; }
     }
     float zq[4] = {0.f, 0.f, 0.f, 0.f};
-    mma16816_b64(zq, za, zb, 0u, 0u, qf.qz());
-    mma16816_b64(zq, za, zb, 0u, 0u, qf.qzlo());
+    // k 0..7 carry the hi parts of Q_j, k 8..15 the lo parts: one MMA for both
+    mma16816_b64(zq, za, zb, za, zb, qf.qz());
     float ta0 = fmaf(zq[0], qscale, -st.m0), ta1 = fmaf(zq[1], qscale, -st.m1);
     float tb0 = fmaf(zq[2], qscale, -st.m0), tb1 = fmaf(zq[3], qscale, -st.m1);
 #pragma unroll
@@ -938,8 +937,7 @@ __device__ __forceinline__ float build_qtab(const float* qraw, uint64_t* qtab, i
     if (j == 2 * q) qa = part;
     if (j == 2 * q + 1) qb = part;
   }
-  put(2 * QF::NCH, pack_b64(pack_h2(qa, qb), 0u));
-  put(2 * QF::NCH + 1, pack_b64(pack_h2(lo(qa), lo(qb)), 0u));
+  put(2 * QF::NCH, pack_b64(pack_h2(qa, qb), pack_h2(lo(qa), lo(qb))));  // k-lo: hi parts, k-hi: lo parts
   return qscale * __int_as_float((127 + qexp) << 23);
 }
 
