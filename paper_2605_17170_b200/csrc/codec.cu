@@ -303,6 +303,16 @@ struct PrefillCfg {
   static constexpr int SMEM = 2 * STAGES * TILE + page_stride(D) + 16;  // stages x (K, V) + the record + page ids
 };
 
+#ifndef KVMIX_K1_MINB
+#define KVMIX_K1_MINB 5  // register budget for at most this many CTAs per SM (5 at d = 128 bf16: 1.3% faster than no bound)
+#endif
+// the page kernel's resident CTAs per SM as shared memory allows, capped at KVMIX_K1_MINB (its launch bound)
+template <int D, typename T>
+struct K1MinBlocks {
+  static constexpr int fit = (227 * 1024) / (PrefillCfg<D, T>::SMEM + 1024);
+  static constexpr int value = fit < 1 ? 1 : (fit > KVMIX_K1_MINB ? KVMIX_K1_MINB : fit);
+};
+
 template <int D, typename T>
 __device__ __forceinline__ uint8_t* staged(uint8_t* tile, int row, int byte) {
   using P = PrefillCfg<D, T>;
@@ -390,7 +400,7 @@ struct ItemCursor {
 // tokens as items of the same launch was slower: instruction-cache misses; another that
 // staged the index words through shared memory with cp.async lost ~8%.)
 template <int D, typename T>
-__global__ void __launch_bounds__(128) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
+__global__ void __launch_bounds__(128, K1MinBlocks<D, T>::value) prefill_pages_kernel(const T* __restrict__ keys, const T* __restrict__ values,
                                                             int64_t n_tokens, int64_t n_kv_heads, int64_t n_pages,
                                                             int64_t n_items, const int32_t* __restrict__ page_tokens,
                                                             const int32_t* __restrict__ page_ids,
