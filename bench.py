@@ -500,7 +500,7 @@ def measure_churned(args, pool, batch, q, out, timer, peak) -> dict:
 
 def measure_decode_step(args, pool, rids, Hq, timer, world) -> dict:
     """e2e: DecodeStep through the public API (host slot pops, device tables + plan, pinned
-    host q / k_new / v_new in, fused append + attention for all layers, outputs back)."""
+    host q / k_new / v_new in, append + attention for all layers, outputs back)."""
     import torch
 
     import paper_2605_17170_b200 as kv
@@ -528,8 +528,12 @@ def measure_decode_step(args, pool, rids, Hq, timer, world) -> dict:
             "host_ms_per_step": 1000.0 * float(np.median(host_s)),
             "what": "DecodeStep.run(): per step the host pops one INT4 slot per request (pool.py:284-306 LIFO), "
                     "then one CUDA graph: slots H2D, K7 device tables + stream-K plan, q/k_new/v_new H2D from pinned "
-                    "memory (8-layer chunks on a side stream), 64 fused append+attention launches, outputs D2H",
-            "gpu_launches_per_step": 1 + args.layers}
+                    "memory (layer chunks on a side stream), "
+                    + (f"{args.layers} fused append+attention launches" if st.fused_append else
+                       f"per {st.chunks[0][1] - st.chunks[0][0]}-layer chunk one batched INT4 append launch before its attention "
+                       f"launches ({args.layers} in all)")
+                    + ", outputs D2H",
+            "gpu_launches_per_step": 1 + args.layers + (0 if st.fused_append else len(st.chunks))}
 
 
 def cpu_leg(args, samples, outs_dev, qs) -> tuple[dict, dict]:
