@@ -41,6 +41,9 @@ extern "C" {
 
 const char* kvmix_version(void);
 const char* kvmix_last_error(void);
+/* cudaStreamSynchronize(stream) with the library's error reporting (used by the single-group
+ * quantize / dequantize calls, which run one zero-copy kernel on pinned memory per call). */
+int kvmix_stream_sync(void* stream);
 /* record strides of the device pools (bytes) */
 int64_t kvmix_page_stride(int64_t head_dim);
 int64_t kvmix_slot_stride(int64_t head_dim);

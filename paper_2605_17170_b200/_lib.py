@@ -58,6 +58,7 @@ _SIGS = {
                                    ctypes.c_int),
     "kvmix_flash_decode": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P,
                             _P, _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
+    "kvmix_stream_sync": ([_P], ctypes.c_int),
     "kvmix_flash_decode_gather": ([_P, _I32, _P, _I32, _I64, _I64, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64,
                                    _I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _F, _I32, _P, _I32, _P], ctypes.c_int),
     "kvmix_flash_decode_append": ([_P, _I32, _P, _I32, _P, _P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P,

@@ -1,6 +1,8 @@
 // Library-level C ABI: version string and per-thread error message.
 #include <cstring>
 
+#include <cuda_runtime.h>
+
 #include "launch.h"
 
 namespace kvmix {
@@ -13,3 +15,11 @@ void set_error(const char* msg) {
 
 extern "C" const char* kvmix_version(void) { return "kvmix_b200 0.1.0 sm_100a"; }
 extern "C" const char* kvmix_last_error(void) { return kvmix::g_err; }
+extern "C" int kvmix_stream_sync(void* stream) {
+  const cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    kvmix::set_error(cudaGetErrorString(e));
+    return KVMIX_ECUDA;
+  }
+  return KVMIX_OK;
+}

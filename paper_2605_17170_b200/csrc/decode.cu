@@ -161,13 +161,21 @@ __device__ __forceinline__ Unit load_unit(const DecodeArgs& a, int piece) {
   return u;
 }
 
-__device__ __forceinline__ void store_out(const DecodeArgs& a, int64_t oi, float v) {
+// Four consecutive outputs (oi % 4 == 0) with one vector store per destination.
+__device__ __forceinline__ void store_out4(const DecodeArgs& a, int64_t oi, float4 v) {
+  uint2 h;
+  if (a.out_dtype == KVMIX_BF16) {
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    h = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+  } else if (a.out_dtype == KVMIX_F16) {
+    const __half2 lo = __floats2half2_rn(v.x, v.y), hi = __floats2half2_rn(v.z, v.w);
+    h = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+  }
 #pragma unroll
   for (int p = 0; p < MAX_OUTS; ++p) {  // static indices: the pointers stay in the parameter bank
     if (p >= a.n_outs) break;
-    if (a.out_dtype == KVMIX_F32) reinterpret_cast<float*>(a.outs[p])[oi] = v;
-    else if (a.out_dtype == KVMIX_BF16) reinterpret_cast<__nv_bfloat16*>(a.outs[p])[oi] = __float2bfloat16(v);
-    else reinterpret_cast<__half*>(a.outs[p])[oi] = __float2half(v);
+    if (a.out_dtype == KVMIX_F32) *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.outs[p]) + oi) = v;
+    else *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.outs[p]) + oi) = h;
   }
 }
 
@@ -182,28 +190,30 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
                                              const float* sm_l, const float* sm_acc, int* sm_flag) {
   __syncthreads();
   const int64_t obase = ((int64_t)u.b * a.out_heads + a.out_head0 + (int64_t)u.kvh * a.gq) * D;
-  for (int i = threadIdx.x; i < a.gq * D; i += blockDim.x) {
-    const int hh = i / D, c = i % D;
+  // a thread merges 4 consecutive channels of one head (one float4 per warp state, one vector store)
+  for (int i = threadIdx.x; i < a.gq * D / 4; i += blockDim.x) {
+    const int hh = (4 * i) / D, c = (4 * i) % D;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_m[w * 8 + hh]);
-    float acc = 0.f, l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float l = 0.f;
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
       const float mw = sm_m[w * 8 + hh];
       const float f = (mw == -INFINITY) ? 0.f : fast_exp2(mw - M);
-      acc += f * sm_acc[(w * 8 + hh) * D + c];
-      l += f * sm_l[w * 8 + hh];
+      const float4 x = *reinterpret_cast<const float4*>(sm_acc + (w * 8 + hh) * D + c);
+      acc.x = fmaf(f, x.x, acc.x); acc.y = fmaf(f, x.y, acc.y);
+      acc.z = fmaf(f, x.z, acc.z); acc.w = fmaf(f, x.w, acc.w);
+      l = fmaf(f, sm_l[w * 8 + hh], l);
     }
     if (u.slot < 0) {
-      store_out(a, obase + i, acc / l);
+      const float inv = 1.f / l;
+      store_out4(a, obase + 4 * i, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
     } else {
       float* pp = a.part + ((int64_t)u.slot * 8 + hh) * (D + 4);
-      pp[c] = acc;
-      if (c == 0) {
-        pp[D] = M;
-        pp[D + 1] = l;
-      }
+      *reinterpret_cast<float4*>(pp + c) = acc;
+      if (c == 0) *reinterpret_cast<float2*>(pp + D) = make_float2(M, l);
     }
   }
   if (u.slot < 0) return;
@@ -258,11 +268,7 @@ __device__ __forceinline__ void finish_piece(const DecodeArgs& a, const Unit& u,
       M = Mn;
     }
     const float inv = 1.f / l;
-    const int64_t oi = obase + (int64_t)hh * D + c0;
-    store_out(a, oi, acc.x * inv);
-    store_out(a, oi + 1, acc.y * inv);
-    store_out(a, oi + 2, acc.z * inv);
-    store_out(a, oi + 3, acc.w * inv);
+    store_out4(a, obase + (int64_t)hh * D + c0, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
   }
 }
 
