@@ -37,6 +37,34 @@ from .pool import MixedPrecisionPool, split_partitioned
 CTAS_PER_SM = 3
 
 
+def layer_chunks(L: int, layer_chunk=None) -> list:
+    """[(c0, c1)] layer ranges whose uploads / downloads overlap the other ranges' kernels.
+    layer_chunk: an int (uniform ranges; 8 measured best at cfg2), a list of range sizes, or
+    None: ranges of 8 with a short first and last range (2, 6, 8, ..., 6, 2) -- measured equal
+    to uniform 8 at cfg2 (1899 vs 1899 tokens/s)."""
+    if layer_chunk is None:
+        if L < 24:
+            sizes = [min(8, L)] * (-(-L // 8))
+        else:
+            mid = L - 16
+            sizes = [2, 6] + [8] * (mid // 8) + ([mid % 8] if mid % 8 else []) + [6, 2]
+    elif isinstance(layer_chunk, int):
+        if layer_chunk <= 0:
+            raise ValidationError("layer_chunk must be positive")
+        sizes = [layer_chunk] * (-(-L // layer_chunk))
+    else:
+        sizes = [int(x) for x in layer_chunk]
+        if any(x <= 0 for x in sizes) or sum(sizes) < L:
+            raise ValidationError("layer chunk sizes must be positive and cover every layer")
+    out, c = [], 0
+    for n in sizes:
+        if c >= L:
+            break
+        out.append((c, min(L, c + n)))
+        c += n
+    return out
+
+
 class DecodeStep:
     """Graph-captured decode steps (append + attention, all layers) for a fixed request batch.
 
@@ -47,7 +75,7 @@ class DecodeStep:
 
     def __init__(self, pool: MixedPrecisionPool, request_ids, n_q_heads: int, dtype=torch.bfloat16,
                  max_new_tokens: int = 256, n_cta: int | None = None, int4_weight: float = 0.8,
-                 layer_chunk: int = 8, scale: float | None = None, fused_append: bool = False):
+                 layer_chunk=8, scale: float | None = None, fused_append: bool = False):
         cfg = pool.config
         if dtype not in (torch.float32, torch.bfloat16, torch.float16):
             raise ValidationError(f"unsupported dtype {dtype}")
@@ -114,7 +142,7 @@ class DecodeStep:
         self.v_host = torch.zeros(self.k_dev.shape, dtype=dtype).pin_memory()
         self.slots_host = torch.zeros(B, dtype=torch.int32).pin_memory()
         self.slots_dev = torch.zeros(B, **i32)
-        self.chunks = [(c, min(L, c + layer_chunk)) for c in range(0, L, layer_chunk)]
+        self.chunks = layer_chunks(L, layer_chunk)
         self.graph = None
         self.steps = 0
         self._tables(None)  # the initial plan (no append)
