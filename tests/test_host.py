@@ -321,3 +321,22 @@ def test_error_mapping():
     with pytest.raises(kv.CapacityError):
         _lib.check(-3)
     _lib.check(0)
+
+
+def test_decode_step_layer_chunks():
+    """DecodeStep's upload / download ranges cover every layer once, in order."""
+    from paper_2605_17170_b200.decode_step import layer_chunks
+
+    for L in (1, 5, 8, 16, 30, 64, 80):
+        for spec in (8, 3, None, [2, 6, 8, 8, 8, 8, 8, 8, 8, 8, 8]):
+            if isinstance(spec, list) and sum(spec) < L:
+                continue
+            ch = layer_chunks(L, spec)
+            assert ch[0][0] == 0 and ch[-1][1] == L
+            assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+            assert all(c1 > c0 for c0, c1 in ch)
+    assert layer_chunks(64, None)[0] == (0, 2) and layer_chunks(64, None)[-1] == (62, 64)
+    with pytest.raises(kv.ValidationError):
+        layer_chunks(10, [2, 2])
+    with pytest.raises(kv.ValidationError):
+        layer_chunks(10, 0)
