@@ -72,6 +72,15 @@ __device__ __forceinline__ void op(uint32_t (&a)[CH][4], float (&c)[CH][4], uint
   } else if constexpr (OP == 19) {  // cvt and an independent HADD2
     asm volatile("{ .reg .b16 t; mov.b32 {t, _}, %0; cvt.rn.f16x2.e4m3x2 %0, t; }" : "+r"(a[i][0]));
     asm volatile("sub.rn.f16x2 %0, %0, %1;" : "+r"(a[i][1]) : "r"(b0));
+  } else if constexpr (OP == 20) {  // one HMMA plus 8 independent LOP3 (overlap of the tensor and ALU pipes)
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                 : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
+                 : "r"(a[i][0]), "r"(a[i][1]), "r"(a[i][2]), "r"(a[i][3]), "r"(b0), "r"(b1));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("lop3.b32 %0, %0, %1, %2, 0xEA;" : "+r"(a[(i + 1 + k) % CH][k & 3]) : "r"(b0), "r"(b1));
+  } else if constexpr (OP == 21) {  // 8 LOP3 alone (same pattern, no HMMA)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("lop3.b32 %0, %0, %1, %2, 0xEA;" : "+r"(a[(i + 1 + k) % CH][k & 3]) : "r"(b0), "r"(b1));
   } else if constexpr (OP == 14) {  // m16n8k8 f16 -> f32
     asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
                  : "+f"(c[i][0]), "+f"(c[i][1]), "+f"(c[i][2]), "+f"(c[i][3])
@@ -146,5 +155,7 @@ int main() {
   run<17>("cvt e4m3x2->f16x2 alone");
   run<18>("cvt + independent lop3");
   run<19>("cvt + independent hadd2");
+  run<20>("hmma + 8 indep lop3");
+  run<21>("8 lop3 (no hmma)");
   return 0;
 }
