@@ -1149,7 +1149,10 @@ __global__ void KVMIX_FUSED_BOUNDS decode_mma_kernel(const DecodeArgs a) {
     }
     if (!COMPUTE) {
       // measurement variant: data movement only (no dequant / MMA)
-    } else if (t < u.npg) {
+#ifndef KVMIX_INT2_LIKELY
+#define KVMIX_INT2_LIKELY 1  // lay the INT2 tile out as the fall-through path (QK, softmax, PV contiguous)
+#endif
+    } else if (KVMIX_INT2_LIKELY ? __builtin_expect(t < u.npg, 1) : (t < u.npg)) {
       float kb0 = 0.f, kb1 = 0.f;
       if (KVMIX_KZBATCH) {
         const int j = k & 15;
