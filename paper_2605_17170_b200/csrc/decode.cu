@@ -9,16 +9,22 @@
 //
 // Tensor-core kernel (variant 0), one warp = one independent flash-decoding stream:
 //  * each warp owns a STAGES-deep smem ring filled by cp.async.bulk (TMA bulk copies,
-//    one 3 KB copy per INT2 page, one per INT4 slot) completing on mbarriers;
+//    one 2.75 KB copy per INT2 page -- the record minus its trailing key zeros -- and one
+//    per run of consecutive INT4 slots) completing on mbarriers;
 //  * QK^T as S^T[token x head] = K[token x ch] . Q^T with mma.sync m16n8k16 (N = 8 =
-//    the GQA group): INT2 key pages fold the per-channel scale into q (q' = q*s per
-//    page) and add the per-page bias sum_c q_c z_c with one extra MMA whose A rows are
-//    the zeros; INT4 keys are dequantised in registers;
+//    the GQA group): INT2 key pages fold the per-channel scale into q (q' = q*s per page,
+//    as an exact fp16 hi + lo pair: two MMAs per chunk) over key codes made NORMAL fp16 by
+//    the hardware e4m3x2 -> f16x2 conversion; the per-page bias sum_c q_c z_c is batched
+//    over 16 pages (their zero points staged into the merge scratch by bulk copies, A rows =
+//    pages); INT4 keys are dequantised per group in fp32;
 //  * P goes C-fragment -> B-fragment with movmatrix;
-//  * PV as O^T[ch x head] = V^T . P'^T with group-pure M tiles so the per-token
-//    group scale folds into P' = p*s, and sum_t p*z comes from an MMA with A = 1;
-//  * codes become fp16 with one LOP3 against the 0x3C00 exponent (1 + code*2^(p-10))
-//    and an exact HSUB2, leaving code * 2^(p-10); the power of two is undone per row.
+//  * PV as O^T[ch x head] = V^T . P'^T with group-pure M tiles so the per-token group scale
+//    folds into P' = p*s; value codes enter in place as fp16 subnormals (one LOP3 per two
+//    codes), the power of two undone per row; sum_t p*z and the softmax sum come from one
+//    MMA per k-step with A = the zeros / ones;
+//  * the piece epilogue merges the warps' states with float4 smem reads (a thread per four
+//    channels of one head) and stores the output -- into up to 8 destinations for the fused
+//    KV-head all-gather -- or a partial that the unit's last-arriving CTA combines.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
