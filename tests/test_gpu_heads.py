@@ -109,10 +109,11 @@ def test_head_shards_vs_oracle(cuda, data):
         assert np.all(err <= ATOL + RTOL * np.abs(ref)), f"request {i}: max abs err {err.max():.3e}"
 
 
-@pytest.mark.parametrize("shards,dtype", [(2, torch.float32), (4, torch.bfloat16), (8, torch.float32)])
-def test_fused_head_gather(cuda, data, shards, dtype):
+@pytest.mark.parametrize("shards,dtype,n_dest", [(2, torch.float32, 3), (4, torch.bfloat16, 3), (8, torch.float32, 3),
+                                                  (8, torch.float16, 8)])
+def test_fused_head_gather(cuda, data, shards, dtype, n_dest):
     """The combine fused into the kernel (kvmix_flash_decode_gather): every shard's decode stores
-    its head slice into all destination buffers -- here three buffers of this process standing in
+    its head slice into all destination buffers -- here 3 or 8 (the maximum) buffers of this process standing in
     for the ranks' NVLink-mapped outputs -- and each buffer ends up equal to the unsharded decode
     (bit for bit under the per-unit schedule, like the all-gather path)."""
     H, Hq, d = data["H"], data["Hq"], data["d"]
@@ -121,7 +122,7 @@ def test_fused_head_gather(cuda, data, shards, dtype):
     q = data["q"][layer]
     B = len(rids)
     ref = decode(full, rids, q, layer, n_cta=1).to(dtype)
-    dests = [torch.full((B, Hq, d), float("nan"), dtype=dtype, device="cuda") for _ in range(3)]
+    dests = [torch.full((B, Hq, d), float("nan"), dtype=dtype, device="cuda") for _ in range(n_dest)]
     for r in range(shards):
         kvh, qh = kvdist.head_slice(H, Hq, r, shards)
         pool, _ = build(data, kvh)
